@@ -1,0 +1,170 @@
+/*
+ * psso.h -- C ABI of the B200-native PSSO hot path (libpsso.so).
+ *
+ * The reference package (arXiv 2110.01470, `sso`) is pure Python and has no
+ * FFI of its own; these entry points are what its Python host code binds
+ * through ctypes.  Each one replaces one reference
+ * interface, cited below as path:line under /root/reference/pkg/src/sso/.
+ *
+ * Conventions
+ *  - Plain C types only.  Device buffers are borrowed raw pointers (the host
+ *    owns them, e.g. as torch tensors); `stream` is a cudaStream_t passed as
+ *    void* (NULL = legacy default stream).
+ *  - Every function returns PSSO_OK (0) or an error code; the message of the
+ *    last error is available from psso_last_error(ctx) (ctx may be NULL for
+ *    context-free entry points; the message is then thread-local).
+ *  - Fitness values (sol_f, p_f, g_f, trajectory) are always float64; the
+ *    position matrices use the configured dtype.
+ *  - Matrices are particle-major (row i = particle i, contiguous), the layout
+ *    the paper calls "stored sequentially" (reference parallel.py:53-60).
+ */
+#ifndef PSSO_H
+#define PSSO_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PSSO_ABI_VERSION 1
+
+/* status codes */
+#define PSSO_OK 0
+#define PSSO_E_INVALID 1     /* bad argument -> Python ValueError (core.py:69-81) */
+#define PSSO_E_CUDA 2        /* CUDA runtime failure */
+#define PSSO_E_NONFINITE 3   /* non-finite fitness -> NonFiniteFitnessError (core.py:43-53) */
+#define PSSO_E_UNSUPPORTED 4 /* shape/dtype outside what the kernels handle */
+
+/* dtype of the position matrices */
+#define PSSO_F64 0
+#define PSSO_F32 1
+
+/* random source */
+#define PSSO_RNG_REFERENCE 0 /* the reference's keyed SplitMix64 (rng.py:27-92), bit-exact */
+#define PSSO_RNG_PHILOX 1    /* Philox4x32-10 counter RNG (benchmark mode) */
+
+/* config flags */
+#define PSSO_FLAG_KEEP_SOL_F 1 /* fused steps also write sol_f for every row (phase-API
+                                  state parity); default: sol_f is written only for
+                                  non-finite rows, saving 8 bytes per row per iteration */
+
+/* objective ids: 1..9 = f1..f9 (benchmarks.py:33); 0 = test probe: Sphere,
+ * except +inf where x[0] > probe_level (fault injection for tests). */
+#define PSSO_FN_PROBE 0
+
+/* replaces: SsoParams (core.py:56-85) + make_function metadata
+ * (benchmarks.py:169-270) + the seed argument of run_parallel (parallel.py:152) */
+typedef struct psso_config {
+    int32_t fn_id;      /* objective id, see above */
+    int32_t dtype;      /* PSSO_F64 | PSSO_F32 */
+    int32_t rng_mode;   /* PSSO_RNG_REFERENCE | PSSO_RNG_PHILOX */
+    int32_t flags;      /* PSSO_FLAG_* bits */
+    int64_t nsol;       /* global swarm size N */
+    int64_t nvar;       /* problem dimension D */
+    int64_t row_lo;     /* first global particle owned by this context */
+    int64_t row_hi;     /* one past the last; [0, nsol) when unsharded */
+    double cw, cp, cg;  /* cumulative branch thresholds, 0 <= cw <= cp <= cg <= 1 */
+    double var_min, var_max;
+    uint64_t seed;      /* masked to 64 bits like rng.py:68 */
+    double probe_level; /* PSSO_FN_PROBE only */
+} psso_config;
+
+/* replaces: the Swarm dataclass (core.py:88-115).  Device pointers, borrowed. */
+typedef struct psso_buffers {
+    void* sol;      /* (row_hi-row_lo) x nvar, dtype          -> Swarm.sol    */
+    void* pbests;   /* (row_hi-row_lo) x nvar, dtype          -> Swarm.pbests */
+    double* sol_f;  /* (row_hi-row_lo) float64, may be NULL   -> Swarm.sol_f  */
+    double* p_f;    /* (row_hi-row_lo) float64                -> Swarm.p_f    */
+    void* gbest;    /* nvar, dtype                            -> Swarm.gbest  */
+    double* g_f;    /* one float64                            -> Swarm.g_f    */
+    double* traj;   /* trajectory indexed by absolute iteration t, may be NULL
+                       -> RunRecord.trajectory (records.py:46)                  */
+} psso_buffers;
+
+typedef struct psso_ctx psso_ctx;
+
+const char* psso_version(void);
+const char* psso_last_error(const psso_ctx* ctx);
+
+/* replaces: run_parallel set-up (parallel.py:164-173): validation, layout,
+ * partition.  Allocates only small scratch (per-CTA candidate slots). */
+int psso_create(const psso_config* cfg, psso_ctx** out);
+void psso_destroy(psso_ctx* ctx);
+
+/* Attach the swarm buffers and the stream every later call enqueues on. */
+int psso_bind(psso_ctx* ctx, const psso_buffers* bufs, void* stream);
+
+/* replaces: core.initialize (core.py:196-210): INIT draws -> positions ->
+ * fitness -> argmin (lowest index) -> gbest/g_f.  Non-finite -> PSSO_E_NONFINITE
+ * reported by psso_check with iteration -1. */
+int psso_init(psso_ctx* ctx);
+
+/* replaces: one iteration of the run_parallel loop (parallel.py:195-212):
+ * fused search + evaluate + pBest kernel, then the gBest stage-2 kernel and
+ * trajectory[t] = g_f.  Asynchronous. */
+int psso_step(psso_ctx* ctx, int64_t t);
+
+/* replaces: the whole loop `for t in range(t0, t0+niter)` (parallel.py:192-212).
+ * Asynchronous; the iterations are replayed from a captured CUDA graph. */
+int psso_run(psso_ctx* ctx, int64_t t0, int64_t niter);
+
+/* Phase API -- replaces search_phase / evaluate_phase / update_pbests_phase /
+ * update_gbest_phase (parallel.py:120-144).  `t < 0` in psso_evaluate means
+ * "iteration None" (the evaluation is not attributed to an iteration). */
+int psso_search(psso_ctx* ctx, int64_t t);
+int psso_evaluate(psso_ctx* ctx, int64_t t);
+int psso_update_pbests(psso_ctx* ctx);
+int psso_update_gbest(psso_ctx* ctx);
+
+/* Sharded (multi-rank) iteration, split around the gBest exchange.
+ * A candidate record is psso_candidate_bytes(cfg) bytes:
+ *   float64 p_f, int64 global index, then nvar elements of dtype (the row).
+ * psso_step_local: fused kernel over this context's rows, then the local
+ * stage-2 reduction, writing this rank's record to `cand` (device).
+ * psso_apply_candidates: lexicographic (p_f, index) min over `ncand` gathered
+ * records, `<=` against g_f, gbest <- winning row, trajectory[t] = g_f.
+ * Replaces the per-slice candidates + `min(candidates)` of parallel.py:199-212. */
+int64_t psso_candidate_bytes(const psso_config* cfg);
+int psso_init_local(psso_ctx* ctx, void* cand);
+int psso_step_local(psso_ctx* ctx, int64_t t, void* cand);
+int psso_apply_candidates(psso_ctx* ctx, int64_t t, const void* cands, int32_t ncand, int32_t is_init);
+
+/* Synchronizes the stream and reports the first non-finite fitness seen so
+ * far as (iteration, particle); iteration -1 = initialization.  Returns
+ * PSSO_E_NONFINITE if there was one (core.py:190-193 semantics). */
+int psso_check(psso_ctx* ctx, int64_t* bad_t, int64_t* bad_i);
+
+/* Number of kernels this context has launched (for launch accounting). */
+int64_t psso_launch_count(const psso_ctx* ctx);
+
+/* Kernel timing for the roofline: while enabled, psso_step / psso_run (which
+ * then launches directly instead of replaying its graph) bracket every fused
+ * tile-kernel launch with CUDA events on the context's stream.
+ * psso_profile_read synchronizes, returns the summed kernel time (ms) and the
+ * number of timed launches, and resets the record. */
+int psso_profile(psso_ctx* ctx, int32_t enable);
+int psso_profile_read(psso_ctx* ctx, double* kernel_ms, int64_t* nlaunch);
+
+/* replaces: RngStream.uniform (rng.py:73-87) on device: out[k] =
+ * u(seed, stream_key, t, particles[k], variables[k]). */
+int psso_rng_uniform(uint64_t seed, uint64_t stream_key, uint64_t t, const uint64_t* particles,
+                     const uint64_t* variables, int64_t n, double* out, void* stream);
+
+/* replaces: BenchmarkFn.__call__ (benchmarks.py:86-94) on device: fitness of
+ * `rows` contiguous rows of length nvar (dtype) into out (float64). */
+int psso_eval_rows(int32_t fn_id, int32_t dtype, int64_t nvar, const void* x, int64_t rows,
+                   double* out, double probe_level, void* stream);
+
+/* replaces: run_parallel (parallel.py:152-233) end to end with HOST buffers:
+ * allocates device state, initializes, runs niter iterations, copies the
+ * trajectory (niter float64), best position (nvar of dtype) and best fitness
+ * back, frees.  wall_s = loop-only device time (parallel.py:190,216). */
+int psso_solve(const psso_config* cfg, int64_t niter, double* traj, void* best_position,
+               double* best_fitness, double* wall_s);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PSSO_H */

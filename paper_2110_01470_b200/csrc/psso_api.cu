@@ -1,0 +1,886 @@
+// psso_api.cu -- C ABI (include/psso.h) of the PSSO hot path, plus the small
+// kernels around the fused tile kernel: gBest stage 2, the sharded candidate
+// records, the unfused phase kernels, the keyed RNG and launch bookkeeping.
+//
+// Reference anchors (/root/reference/pkg/src/sso/): run_parallel
+// parallel.py:152-233; phases parallel.py:120-144; initialize core.py:196-210;
+// RngStream.uniform rng.py:73-87; BenchmarkFn.__call__ benchmarks.py:86-94.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "psso.h"
+#include "psso_device.cuh"
+#include "psso_registry.h"
+
+using namespace psso;
+
+namespace {
+
+thread_local std::string g_err;
+
+constexpr int GB_THREADS = 256;
+constexpr int GRAPH_CHUNK = 16;  // iterations per captured graph
+
+struct Layout {
+  int V, R, G, S, NL;
+  size_t smem;
+  int off_xs, off_scr, off_gb, off_hb, off_hf, off_leaf, off_rowf, off_flag, off_red;
+  Plan plan;
+};
+
+FastDiv make_div(uint32_t d) {
+  FastDiv f;
+  f.d = d;
+  uint32_t l = 0;
+  while ((1ull << l) < d) ++l;
+  f.s = l;
+  f.m = (uint32_t)(((1ull << 32) * ((1ull << l) - d)) / d + 1);
+  return f;
+}
+
+// numpy add.reduce recursion (pairwise blocks of <= 128, split at n/2 rounded
+// down to a multiple of 8) flattened into leaves + a post-order program.
+bool build_plan(int64_t n, Plan& p, std::string& err) {
+  std::memset(&p, 0, sizeof(p));
+  p.n = (int32_t)n;
+  struct Rec {
+    static bool go(Plan& p, int64_t off, int64_t n) {
+      if (n <= 128) {
+        if (p.nleaves >= MAX_LEAVES || p.nops >= MAX_OPS) return false;
+        p.leaf_off[p.nleaves] = (int32_t)off;
+        p.leaf_len[p.nleaves] = (int32_t)n;
+        p.ops[p.nops++] = (int8_t)p.nleaves;
+        p.nleaves++;
+        return true;
+      }
+      int64_t n2 = n / 2;
+      n2 -= n2 % 8;
+      if (!go(p, off, n2) || !go(p, off + n2, n - n2)) return false;
+      if (p.nops >= MAX_OPS) return false;
+      p.ops[p.nops++] = -1;
+      return true;
+    }
+  };
+  if (!Rec::go(p, 0, n)) {
+    err = "row reduction needs more than " + std::to_string(MAX_LEAVES) + " pairwise leaves";
+    return false;
+  }
+  return true;
+}
+
+int64_t terms_of(int fn, int64_t D) {
+  if (fn == 4) return D - 1;
+  if (fn == 8) return D / 4;
+  return D;
+}
+
+size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+bool make_layout(int fn, int dtype, int64_t D, Layout& L, std::string& err) {
+  const int es = dtype == PSSO_F64 ? 8 : 4;
+  if (!build_plan(terms_of(fn, D), L.plan, err)) return false;
+  L.NL = L.plan.nleaves;
+  L.G = 8 * L.NL;
+  L.V = dtype == PSSO_F64 ? (D % 2 == 0 ? 2 : 1) : (D % 4 == 0 ? 4 : 1);
+  const int mod = dtype == PSSO_F64 ? 16 : 32;
+  int64_t S = D;
+  while (S % mod != 8 % mod || S % L.V) ++S;  // chain reads conflict-free
+  L.S = (int)S;
+  const bool scr = (fn == 3 || fn == 7);
+  const size_t fixed = align16(D * es) + 128;
+  auto smem_for = [&](int R) {
+    size_t s = align16((size_t)R * S * es);        // xs
+    s += scr ? align16((size_t)R * S * 8) : 0;     // scratch
+    s += align16(D * es);                          // gbest
+    s += 2 * align16((size_t)R * 8);               // hashes
+    s += align16((size_t)R * L.NL * 16);           // leaf values
+    s += align16((size_t)R * 8) + align16((size_t)R * 4) + 128;
+    return s;
+  };
+  (void)fixed;
+  int R = L.G >= NT ? 1 : NT / L.G;
+  const size_t cap = 200 * 1024;
+  while (R > 1 && smem_for(R) > cap) R /= 2;
+  if (smem_for(R) > 227 * 1024) {
+    err = "nvar " + std::to_string(D) + " too large for the shared-memory row tile";
+    return false;
+  }
+  L.R = R;
+  size_t o = 0;
+  L.off_xs = (int)o; o += align16((size_t)R * S * es);
+  L.off_scr = (int)o; o += scr ? align16((size_t)R * S * 8) : 0;
+  L.off_gb = (int)o; o += align16(D * es);
+  L.off_hb = (int)o; o += align16((size_t)R * 8);
+  L.off_hf = (int)o; o += align16((size_t)R * 8);
+  L.off_leaf = (int)o; o += align16((size_t)R * L.NL * 16);
+  L.off_rowf = (int)o; o += align16((size_t)R * 8);
+  L.off_flag = (int)o; o += align16((size_t)R * 4);
+  L.off_red = (int)o; o += 128;
+  L.smem = o;
+  return true;
+}
+
+uint64_t k53(double c) {  // (h >> 11) * 2^-53 < c  <=>  (h >> 11) < ceil(c * 2^53)
+  double y = std::ceil(c * 9007199254740992.0);
+  if (y <= 0.0) return 0;
+  if (y >= 9007199254740992.0) return 1ull << 53;
+  return (uint64_t)y;
+}
+uint64_t k32(double c) {
+  double y = std::ceil(c * 4294967296.0);
+  if (y <= 0.0) return 0;
+  if (y >= 4294967296.0) return 1ull << 32;
+  return (uint64_t)y;
+}
+
+// ------------------------------------------------------------ kernels ----
+
+struct GbParams {
+  const double* slot_f;
+  const int64_t* slot_i;
+  int32_t nslots;
+  int32_t D;
+  const void* P;         // local pbests
+  int64_t row_lo;
+  void* gbest;
+  double* g_f;
+  double* traj;          // may be null
+  int64_t t_arg;
+  int64_t* t_dev;        // if non-null: t read here and incremented
+  int32_t is_init;
+  int32_t pad;
+};
+
+template <typename T>
+__device__ void block_argmin(const double* f, const int64_t* idx, int n, double& bf, int64_t& bi,
+                             double* sf, int64_t* si) {
+  bf = CUDART_INF;
+  bi = INT64_MAX;
+  for (int k = threadIdx.x; k < n; k += blockDim.x)
+    if (lex_less(f[k], idx[k], bf, bi)) { bf = f[k]; bi = idx[k]; }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double of = __shfl_xor_sync(0xffffffffu, bf, o);
+    int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (lex_less(of, oi, bf, bi)) { bf = of; bi = oi; }
+  }
+  if ((threadIdx.x & 31) == 0) { sf[threadIdx.x >> 5] = bf; si[threadIdx.x >> 5] = bi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      if (lex_less(sf[w], si[w], sf[0], si[0])) { sf[0] = sf[w]; si[0] = si[w]; }
+  }
+  __syncthreads();
+  bf = sf[0];
+  bi = si[0];
+}
+
+// gBest stage 2 (parallel.py:208-212): deterministic lexicographic min over
+// the per-CTA slots, `<=` against the incumbent, winner row -> gbest.
+template <typename T>
+__global__ void __launch_bounds__(GB_THREADS) k_gbest(const __grid_constant__ GbParams g) {
+  __shared__ double sf[GB_THREADS / 32];
+  __shared__ int64_t si[GB_THREADS / 32];
+  double bf;
+  int64_t bi;
+  block_argmin<T>(g.slot_f, g.slot_i, g.nslots, bf, bi, sf, si);
+  const double inc = *g.g_f;
+  const bool take = bi != INT64_MAX && (g.is_init || bf <= inc);
+  if (take) {
+    const T* src = reinterpret_cast<const T*>(g.P) + (bi - g.row_lo) * (int64_t)g.D;
+    T* dst = reinterpret_cast<T*>(g.gbest);
+    for (int j = threadIdx.x; j < g.D; j += blockDim.x) dst[j] = src[j];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double gf = take ? bf : inc;
+    if (take) *g.g_f = gf;
+    const int64_t t = g.t_dev ? *g.t_dev : g.t_arg;
+    if (g.traj && t >= 0) g.traj[t] = gf;
+    if (g.t_dev) *g.t_dev = t + 1;
+  }
+}
+
+// Local stage 2 for sharded runs: this rank's (p_f, index, row) record.
+template <typename T>
+__global__ void __launch_bounds__(GB_THREADS) k_local_cand(const __grid_constant__ GbParams g,
+                                                           unsigned char* rec) {
+  __shared__ double sf[GB_THREADS / 32];
+  __shared__ int64_t si[GB_THREADS / 32];
+  double bf;
+  int64_t bi;
+  block_argmin<T>(g.slot_f, g.slot_i, g.nslots, bf, bi, sf, si);
+  if (bi != INT64_MAX) {
+    const T* src = reinterpret_cast<const T*>(g.P) + (bi - g.row_lo) * (int64_t)g.D;
+    T* dst = reinterpret_cast<T*>(rec + 16);
+    for (int j = threadIdx.x; j < g.D; j += blockDim.x) dst[j] = src[j];
+  }
+  if (threadIdx.x == 0) {
+    *reinterpret_cast<double*>(rec) = bf;
+    *reinterpret_cast<int64_t*>(rec + 8) = bi;
+  }
+}
+
+// Global stage 2 over gathered records (one per rank, in rank order).
+template <typename T>
+__global__ void __launch_bounds__(GB_THREADS) k_apply(const __grid_constant__ GbParams g,
+                                                      const unsigned char* recs, int64_t rec_bytes,
+                                                      int ncand) {
+  __shared__ int winner;
+  __shared__ int take_s;
+  if (threadIdx.x == 0) {
+    double bf = CUDART_INF;
+    int64_t bi = INT64_MAX;
+    int w = 0;
+    for (int k = 0; k < ncand; ++k) {
+      const unsigned char* r = recs + k * rec_bytes;
+      double f = *reinterpret_cast<const double*>(r);
+      int64_t i = *reinterpret_cast<const int64_t*>(r + 8);
+      if (lex_less(f, i, bf, bi)) { bf = f; bi = i; w = k; }
+    }
+    const double inc = *g.g_f;
+    take_s = bi != INT64_MAX && (g.is_init || bf <= inc);
+    winner = w;
+    const double gf = take_s ? bf : inc;
+    if (take_s) *g.g_f = gf;
+    const int64_t t = g.t_dev ? *g.t_dev : g.t_arg;
+    if (g.traj && t >= 0) g.traj[t] = gf;
+    if (g.t_dev) *g.t_dev = t + 1;
+  }
+  __syncthreads();
+  if (take_s) {
+    const T* src = reinterpret_cast<const T*>(recs + winner * rec_bytes + 16);
+    T* dst = reinterpret_cast<T*>(g.gbest);
+    for (int j = threadIdx.x; j < g.D; j += blockDim.x) dst[j] = src[j];
+  }
+}
+
+// per-CTA argmin of p_f over local rows (update_gbest_phase, parallel.py:138-144)
+__global__ void k_argmin(const double* f, int64_t n, int64_t row_lo, double* slot_f,
+                         int64_t* slot_i) {
+  __shared__ double sf[32];
+  __shared__ int64_t si[32];
+  double bf = CUDART_INF;
+  int64_t bi = INT64_MAX;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    if (lex_less(f[k], row_lo + k, bf, bi)) { bf = f[k]; bi = row_lo + k; }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double of = __shfl_xor_sync(0xffffffffu, bf, o);
+    int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (lex_less(of, oi, bf, bi)) { bf = of; bi = oi; }
+  }
+  if ((threadIdx.x & 31) == 0) { sf[threadIdx.x >> 5] = bf; si[threadIdx.x >> 5] = bi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      if (lex_less(sf[w], si[w], bf, bi)) { bf = sf[w]; bi = si[w]; }
+    slot_f[blockIdx.x] = bf;
+    slot_i[blockIdx.x] = bi;
+  }
+}
+
+// update_pbests_phase (parallel.py:132-135): sol_f <= p_f -> copy row.
+template <typename T>
+__global__ void k_pbest(const T* X, T* P, const double* sol_f, double* p_f, int64_t rows, int D) {
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const bool imp = sol_f[r] <= p_f[r];
+    if (!imp) continue;
+    for (int j = threadIdx.x; j < D; j += blockDim.x) P[r * D + j] = X[r * D + j];
+    __syncthreads();
+    if (threadIdx.x == 0) p_f[r] = sol_f[r];
+  }
+}
+
+__global__ void k_rng(uint64_t seed, uint64_t stream, uint64_t t, const uint64_t* ii,
+                      const uint64_t* jj, int64_t n, double* out) {
+  const uint64_t root = root64(seed, stream, t);
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    out[k] = unit53(fold64(fold64(root, ii[k]), jj[k]));
+}
+
+__global__ void k_inv_sqrt(double* aux, int D) {  // 1.0 / np.sqrt(np.arange(1, D+1))
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < D; j += gridDim.x * blockDim.x)
+    aux[j] = __ddiv_rn(1.0, __dsqrt_rn((double)(j + 1)));
+}
+
+__global__ void k_set(int64_t* p, int64_t v) { *p = v; }
+__global__ void k_set_u64(unsigned long long* p, unsigned long long v) { *p = v; }
+
+}  // namespace
+
+// ------------------------------------------------------------- context ----
+
+struct psso_ctx {
+  psso_config cfg;
+  psso_buffers buf;
+  bool bound;
+  cudaStream_t stream;
+  int device, num_sms;
+  Layout L;
+  const void* tile_fn;
+  int grid;
+  int argmin_grid;
+  int nslots;
+  double* slot_f;
+  int64_t* slot_i;
+  unsigned long long* bad;
+  int64_t* t_dev;
+  double* aux;
+  uint64_t Kw, Kp, Kg, Kw32, Kp32, Kg32;
+  int64_t launches;
+  cudaGraphExec_t graph;
+  // kernel timing (psso_profile): event pairs around each fused tile launch
+  bool profiling;
+  std::vector<cudaEvent_t> ev;
+  size_t ev_used;
+  std::string err;
+};
+
+namespace {
+
+int fail(psso_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(psso_ctx* c, cudaError_t e, const char* where) {
+  return fail(c, PSSO_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(ctx, call)                                  \
+  do {                                                 \
+    cudaError_t e_ = (call);                           \
+    if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call); \
+  } while (0)
+
+int validate(const psso_config* c, std::string& err) {
+  if (!c) { err = "null config"; return PSSO_E_INVALID; }
+  if (c->fn_id < 0 || c->fn_id > 9) { err = "unknown function id " + std::to_string(c->fn_id); return PSSO_E_INVALID; }
+  if (c->dtype != PSSO_F64 && c->dtype != PSSO_F32) { err = "dtype must be PSSO_F64 or PSSO_F32"; return PSSO_E_INVALID; }
+  if (c->rng_mode != PSSO_RNG_REFERENCE && c->rng_mode != PSSO_RNG_PHILOX) { err = "unknown rng_mode"; return PSSO_E_INVALID; }
+  if (!(0.0 <= c->cw && c->cw <= c->cp && c->cp <= c->cg && c->cg <= 1.0)) {
+    char b[160];
+    std::snprintf(b, sizeof b, "thresholds must satisfy 0 <= cw <= cp <= cg <= 1, got (%.17g, %.17g, %.17g)", c->cw, c->cp, c->cg);
+    err = b;
+    return PSSO_E_INVALID;
+  }
+  if (!(c->var_min < c->var_max)) { err = "need var_min < var_max"; return PSSO_E_INVALID; }
+  if (c->nsol < 1) { err = "nsol must be a positive integer"; return PSSO_E_INVALID; }
+  if (c->nvar < 1) { err = "nvar must be a positive integer"; return PSSO_E_INVALID; }
+  if (c->fn_id == 4 && c->nvar < 2) { err = "f4 needs dimension >= 2"; return PSSO_E_INVALID; }
+  if (c->fn_id == 8 && c->nvar < 4) { err = "f8 needs at least 4 variables"; return PSSO_E_INVALID; }
+  if (!(0 <= c->row_lo && c->row_lo < c->row_hi && c->row_hi <= c->nsol)) { err = "row range must satisfy 0 <= row_lo < row_hi <= nsol"; return PSSO_E_INVALID; }
+  if (c->nvar > (1 << 20)) { err = "nvar too large"; return PSSO_E_UNSUPPORTED; }
+  if (c->flags & ~PSSO_FLAG_KEEP_SOL_F) { err = "unknown flags"; return PSSO_E_INVALID; }
+  return PSSO_OK;
+}
+
+TileParams tile_params(psso_ctx* c, int mode, int64_t t, const int64_t* t_dev) {
+  TileParams p;
+  std::memset(&p, 0, sizeof(p));
+  const Layout& L = c->L;
+  p.X = c->buf.sol;
+  p.P = c->buf.pbests;
+  p.sol_f = c->buf.sol_f;
+  p.p_f = c->buf.p_f;
+  p.gbest = c->buf.gbest;
+  p.rows = c->cfg.row_hi - c->cfg.row_lo;
+  p.row_lo = c->cfg.row_lo;
+  p.D = (int32_t)c->cfg.nvar;
+  p.R = L.R;
+  p.G = L.G;
+  p.S = L.S;
+  p.cpr = (int32_t)(c->cfg.nvar / L.V);
+  p.mode = mode;
+  p.div_cpr = make_div((uint32_t)p.cpr);
+  p.div_G = make_div((uint32_t)L.G);
+  p.div_D = make_div((uint32_t)c->cfg.nvar);
+  p.seed = c->cfg.seed;
+  p.Kw = c->Kw; p.Kp = c->Kp; p.Kg = c->Kg;
+  p.Kw32 = c->Kw32; p.Kp32 = c->Kp32; p.Kg32 = c->Kg32;
+  p.var_min = c->cfg.var_min;
+  p.span = c->cfg.var_max - c->cfg.var_min;
+  p.probe_level = c->cfg.probe_level;
+  p.t_arg = t;
+  p.t_dev = t_dev;
+  p.slot_f = c->slot_f;
+  p.slot_i = c->slot_i;
+  p.bad = c->bad;
+  p.aux = c->aux;
+  p.off_xs = L.off_xs; p.off_scr = L.off_scr; p.off_gb = L.off_gb; p.off_hb = L.off_hb;
+  p.off_hf = L.off_hf; p.off_leaf = L.off_leaf; p.off_rowf = L.off_rowf; p.off_flag = L.off_flag;
+  p.off_red = L.off_red;
+  p.plan = L.plan;
+  return p;
+}
+
+int launch_tile(psso_ctx* c, const TileParams& p) {
+  void* args[] = {(void*)&p};
+  CK(c, cudaLaunchKernel(c->tile_fn, dim3(c->grid), dim3(NT), args, c->L.smem, c->stream));
+  c->launches++;
+  return PSSO_OK;
+}
+
+GbParams gb_params(psso_ctx* c, int64_t t, int64_t* t_dev, int is_init, int nslots) {
+  GbParams g;
+  std::memset(&g, 0, sizeof(g));
+  g.slot_f = c->slot_f;
+  g.slot_i = c->slot_i;
+  g.nslots = nslots;
+  g.D = (int32_t)c->cfg.nvar;
+  g.P = c->buf.pbests;
+  g.row_lo = c->cfg.row_lo;
+  g.gbest = c->buf.gbest;
+  g.g_f = c->buf.g_f;
+  g.traj = c->buf.traj;
+  g.t_arg = t;
+  g.t_dev = t_dev;
+  g.is_init = is_init;
+  return g;
+}
+
+int launch_gbest(psso_ctx* c, const GbParams& g) {
+  void* args[] = {(void*)&g};
+  const void* fn = c->cfg.dtype == PSSO_F64 ? (const void*)k_gbest<double> : (const void*)k_gbest<float>;
+  CK(c, cudaLaunchKernel(fn, dim3(1), dim3(GB_THREADS), args, 0, c->stream));
+  c->launches++;
+  return PSSO_OK;
+}
+
+int need_bound(psso_ctx* c) {
+  if (!c) return fail(nullptr, PSSO_E_INVALID, "null context");
+  if (!c->bound) return fail(c, PSSO_E_INVALID, "context has no buffers bound (psso_bind)");
+  return PSSO_OK;
+}
+
+int fused_mode(const psso_ctx* c) {
+  return M_SEARCH | M_EVAL | M_PBEST | M_CAND | ((c->cfg.flags & PSSO_FLAG_KEEP_SOL_F) ? M_SOLF : 0);
+}
+
+// the fused tile kernel, bracketed by timing events while profiling
+int launch_fused(psso_ctx* c, int64_t t, int64_t* t_dev) {
+  const bool timed = c->profiling && !t_dev;
+  if (timed) {
+    if (c->ev_used + 2 > c->ev.size()) {
+      for (int k = 0; k < 64; ++k) {
+        cudaEvent_t e;
+        CK(c, cudaEventCreate(&e));
+        c->ev.push_back(e);
+      }
+    }
+    CK(c, cudaEventRecord(c->ev[c->ev_used], c->stream));
+  }
+  int rc = launch_tile(c, tile_params(c, fused_mode(c), t, t_dev));
+  if (rc) return rc;
+  if (timed) {
+    CK(c, cudaEventRecord(c->ev[c->ev_used + 1], c->stream));
+    c->ev_used += 2;
+  }
+  return PSSO_OK;
+}
+
+int fused_step(psso_ctx* c, int64_t t, int64_t* t_dev) {
+  if (int rc = launch_fused(c, t, t_dev)) return rc;
+  return launch_gbest(c, gb_params(c, t, t_dev, 0, c->grid));
+}
+
+}  // namespace
+
+// ------------------------------------------------------------- C ABI ----
+
+extern "C" {
+
+const char* psso_version(void) { return "psso-b200 1 (sm_100a)"; }
+
+const char* psso_last_error(const psso_ctx* ctx) {
+  if (ctx && !ctx->err.empty()) return ctx->err.c_str();
+  return g_err.c_str();
+}
+
+int psso_create(const psso_config* cfg, psso_ctx** out) {
+  std::string err;
+  if (!out) return fail(nullptr, PSSO_E_INVALID, "null output pointer");
+  *out = nullptr;
+  int rc = validate(cfg, err);
+  if (rc) return fail(nullptr, rc, err);
+  psso_ctx* c = new psso_ctx();
+  c->cfg = *cfg;
+  c->bound = false;
+  c->stream = nullptr;
+  c->graph = nullptr;
+  c->launches = 0;
+  c->profiling = false;
+  c->ev_used = 0;
+  if (!make_layout(cfg->fn_id, cfg->dtype, cfg->nvar, c->L, err)) {
+    delete c;
+    return fail(nullptr, PSSO_E_UNSUPPORTED, err);
+  }
+  c->tile_fn = tile_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, c->L.V);
+  if (!c->tile_fn) {
+    delete c;
+    return fail(nullptr, PSSO_E_UNSUPPORTED, "no kernel instantiation for this configuration");
+  }
+  cudaError_t e;
+  if ((e = cudaGetDevice(&c->device)) != cudaSuccess ||
+      (e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device)) != cudaSuccess ||
+      (e = cudaFuncSetAttribute(c->tile_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->L.smem)) != cudaSuccess) {
+    delete c;
+    return cuda_fail(nullptr, e, "psso_create");
+  }
+  int per_sm = 0;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, c->tile_fn, NT, c->L.smem)) != cudaSuccess || per_sm < 1) {
+    delete c;
+    return e != cudaSuccess ? cuda_fail(nullptr, e, "occupancy") : fail(nullptr, PSSO_E_UNSUPPORTED, "tile kernel cannot be resident");
+  }
+  const int64_t rows = cfg->row_hi - cfg->row_lo;
+  const int64_t ntiles = (rows + c->L.R - 1) / c->L.R;
+  c->grid = (int)std::min<int64_t>(ntiles, (int64_t)per_sm * c->num_sms);
+  c->argmin_grid = (int)std::min<int64_t>((rows + 255) / 256, 4 * c->num_sms);
+  c->nslots = std::max(c->grid, c->argmin_grid);
+  c->Kw = k53(cfg->cw); c->Kp = k53(cfg->cp); c->Kg = k53(cfg->cg);
+  c->Kw32 = k32(cfg->cw); c->Kp32 = k32(cfg->cp); c->Kg32 = k32(cfg->cg);
+  c->aux = nullptr;
+  if ((e = cudaMalloc(&c->slot_f, sizeof(double) * c->nslots)) != cudaSuccess ||
+      (e = cudaMalloc(&c->slot_i, sizeof(int64_t) * c->nslots)) != cudaSuccess ||
+      (e = cudaMalloc(&c->bad, sizeof(unsigned long long))) != cudaSuccess ||
+      (e = cudaMalloc(&c->t_dev, sizeof(int64_t))) != cudaSuccess ||
+      (e = cudaMemset(c->bad, 0xff, sizeof(unsigned long long))) != cudaSuccess) {
+    psso_destroy(c);
+    return cuda_fail(nullptr, e, "psso_create alloc");
+  }
+  if (cfg->fn_id == 7) {
+    if ((e = cudaMalloc(&c->aux, sizeof(double) * cfg->nvar)) != cudaSuccess) {
+      psso_destroy(c);
+      return cuda_fail(nullptr, e, "psso_create aux");
+    }
+    k_inv_sqrt<<<(int)((cfg->nvar + 255) / 256), 256>>>(c->aux, (int)cfg->nvar);
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) {
+      psso_destroy(c);
+      return cuda_fail(nullptr, e, "psso_create aux init");
+    }
+  }
+  *out = c;
+  return PSSO_OK;
+}
+
+void psso_destroy(psso_ctx* c) {
+  if (!c) return;
+  if (c->graph) cudaGraphExecDestroy(c->graph);
+  for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+  cudaFree(c->slot_f);
+  cudaFree(c->slot_i);
+  cudaFree(c->bad);
+  cudaFree(c->t_dev);
+  cudaFree(c->aux);
+  delete c;
+}
+
+int psso_bind(psso_ctx* c, const psso_buffers* b, void* stream) {
+  if (!c) return fail(nullptr, PSSO_E_INVALID, "null context");
+  if (!b || !b->sol || !b->pbests || !b->p_f || !b->gbest || !b->g_f)
+    return fail(c, PSSO_E_INVALID, "sol, pbests, p_f, gbest and g_f buffers are required");
+  const uintptr_t al = 16;
+  if (((uintptr_t)b->sol | (uintptr_t)b->pbests | (uintptr_t)b->gbest) % al)
+    return fail(c, PSSO_E_INVALID, "position buffers must be 16-byte aligned");
+  c->buf = *b;
+  c->stream = (cudaStream_t)stream;
+  c->bound = true;
+  if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }
+  return PSSO_OK;
+}
+
+int psso_init(psso_ctx* c) {
+  if (int rc = need_bound(c)) return rc;
+  k_set_u64<<<1, 1, 0, c->stream>>>(c->bad, ~0ull);
+  c->launches++;
+  int rc = launch_tile(c, tile_params(c, M_INIT | M_EVAL | M_CAND | M_SOLF, -1, nullptr));
+  if (rc) return rc;
+  GbParams g = gb_params(c, -1, nullptr, 1, c->grid);
+  g.traj = nullptr;
+  return launch_gbest(c, g);
+}
+
+int psso_step(psso_ctx* c, int64_t t) {
+  if (int rc = need_bound(c)) return rc;
+  if (t < 0) return fail(c, PSSO_E_INVALID, "iteration must be >= 0");
+  return fused_step(c, t, nullptr);
+}
+
+int psso_run(psso_ctx* c, int64_t t0, int64_t niter) {
+  if (int rc = need_bound(c)) return rc;
+  if (t0 < 0 || niter < 0) return fail(c, PSSO_E_INVALID, "t0 and niter must be >= 0");
+  int64_t done = 0;
+  if (c->stream != nullptr && niter >= GRAPH_CHUNK && !c->profiling) {
+    if (!c->graph) {  // capture GRAPH_CHUNK fused iterations, t read from t_dev
+      cudaGraph_t g;
+      CK(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+      int64_t saved = c->launches;
+      for (int k = 0; k < GRAPH_CHUNK; ++k) {
+        int rc = fused_step(c, 0, c->t_dev);
+        if (rc) { cudaStreamEndCapture(c->stream, &g); return rc; }
+      }
+      c->launches = saved;
+      CK(c, cudaStreamEndCapture(c->stream, &g));
+      cudaError_t e = cudaGraphInstantiate(&c->graph, g, 0);
+      cudaGraphDestroy(g);
+      if (e != cudaSuccess) return cuda_fail(c, e, "cudaGraphInstantiate");
+    }
+    k_set<<<1, 1, 0, c->stream>>>(c->t_dev, t0);
+    c->launches++;
+    for (; done + GRAPH_CHUNK <= niter; done += GRAPH_CHUNK) {
+      CK(c, cudaGraphLaunch(c->graph, c->stream));
+      c->launches += 2 * GRAPH_CHUNK;
+    }
+  }
+  for (; done < niter; ++done) {
+    int rc = fused_step(c, t0 + done, nullptr);
+    if (rc) return rc;
+  }
+  return PSSO_OK;
+}
+
+int psso_search(psso_ctx* c, int64_t t) {
+  if (int rc = need_bound(c)) return rc;
+  return launch_tile(c, tile_params(c, M_SEARCH, t, nullptr));
+}
+
+int psso_evaluate(psso_ctx* c, int64_t t) {
+  if (int rc = need_bound(c)) return rc;
+  if (!c->buf.sol_f) return fail(c, PSSO_E_INVALID, "evaluate needs a sol_f buffer");
+  return launch_tile(c, tile_params(c, M_LOAD | M_EVAL | M_SOLF, t < 0 ? -1 : t, nullptr));
+}
+
+int psso_update_pbests(psso_ctx* c) {
+  if (int rc = need_bound(c)) return rc;
+  if (!c->buf.sol_f) return fail(c, PSSO_E_INVALID, "update_pbests needs a sol_f buffer");
+  const int64_t rows = c->cfg.row_hi - c->cfg.row_lo;
+  const int grid = (int)std::min<int64_t>(rows, 8 * c->num_sms);
+  if (c->cfg.dtype == PSSO_F64)
+    k_pbest<double><<<grid, 128, 0, c->stream>>>((const double*)c->buf.sol, (double*)c->buf.pbests,
+                                                 c->buf.sol_f, c->buf.p_f, rows, (int)c->cfg.nvar);
+  else
+    k_pbest<float><<<grid, 128, 0, c->stream>>>((const float*)c->buf.sol, (float*)c->buf.pbests,
+                                                c->buf.sol_f, c->buf.p_f, rows, (int)c->cfg.nvar);
+  c->launches++;
+  CK(c, cudaGetLastError());
+  return PSSO_OK;
+}
+
+int psso_update_gbest(psso_ctx* c) {
+  if (int rc = need_bound(c)) return rc;
+  const int64_t rows = c->cfg.row_hi - c->cfg.row_lo;
+  k_argmin<<<c->argmin_grid, 256, 0, c->stream>>>(c->buf.p_f, rows, c->cfg.row_lo, c->slot_f, c->slot_i);
+  c->launches++;
+  CK(c, cudaGetLastError());
+  GbParams g = gb_params(c, -1, nullptr, 0, c->argmin_grid);
+  g.traj = nullptr;
+  return launch_gbest(c, g);
+}
+
+int64_t psso_candidate_bytes(const psso_config* cfg) {
+  if (!cfg) return -1;
+  const int64_t es = cfg->dtype == PSSO_F64 ? 8 : 4;
+  return 16 + ((cfg->nvar * es + 15) / 16) * 16;
+}
+
+static int local_cand(psso_ctx* c, void* cand) {
+  GbParams g = gb_params(c, -1, nullptr, 0, c->grid);
+  unsigned char* rec = (unsigned char*)cand;
+  if (c->cfg.dtype == PSSO_F64)
+    k_local_cand<double><<<1, GB_THREADS, 0, c->stream>>>(g, rec);
+  else
+    k_local_cand<float><<<1, GB_THREADS, 0, c->stream>>>(g, rec);
+  c->launches++;
+  CK(c, cudaGetLastError());
+  return PSSO_OK;
+}
+
+int psso_init_local(psso_ctx* c, void* cand) {
+  if (int rc = need_bound(c)) return rc;
+  if (!cand) return fail(c, PSSO_E_INVALID, "null candidate buffer");
+  k_set_u64<<<1, 1, 0, c->stream>>>(c->bad, ~0ull);
+  c->launches++;
+  int rc = launch_tile(c, tile_params(c, M_INIT | M_EVAL | M_CAND | M_SOLF, -1, nullptr));
+  if (rc) return rc;
+  return local_cand(c, cand);
+}
+
+int psso_step_local(psso_ctx* c, int64_t t, void* cand) {
+  if (int rc = need_bound(c)) return rc;
+  if (!cand) return fail(c, PSSO_E_INVALID, "null candidate buffer");
+  if (int rc = launch_fused(c, t, nullptr)) return rc;
+  return local_cand(c, cand);
+}
+
+int psso_apply_candidates(psso_ctx* c, int64_t t, const void* cands, int32_t ncand, int32_t is_init) {
+  if (int rc = need_bound(c)) return rc;
+  if (!cands || ncand < 1) return fail(c, PSSO_E_INVALID, "need at least one candidate record");
+  GbParams g = gb_params(c, t, nullptr, is_init, 0);
+  if (is_init) g.traj = nullptr;
+  const int64_t rb = psso_candidate_bytes(&c->cfg);
+  if (c->cfg.dtype == PSSO_F64)
+    k_apply<double><<<1, GB_THREADS, 0, c->stream>>>(g, (const unsigned char*)cands, rb, ncand);
+  else
+    k_apply<float><<<1, GB_THREADS, 0, c->stream>>>(g, (const unsigned char*)cands, rb, ncand);
+  c->launches++;
+  CK(c, cudaGetLastError());
+  return PSSO_OK;
+}
+
+int psso_check(psso_ctx* c, int64_t* bad_t, int64_t* bad_i) {
+  if (!c) return fail(nullptr, PSSO_E_INVALID, "null context");
+  unsigned long long key = ~0ull;
+  CK(c, cudaStreamSynchronize(c->stream));
+  CK(c, cudaMemcpy(&key, c->bad, sizeof key, cudaMemcpyDeviceToHost));
+  if (key == ~0ull) {
+    if (bad_t) *bad_t = 0;
+    if (bad_i) *bad_i = -1;
+    return PSSO_OK;
+  }
+  if (bad_t) *bad_t = (int64_t)(key >> 40) - 1;
+  if (bad_i) *bad_i = (int64_t)(key & ((1ull << 40) - 1));
+  return fail(c, PSSO_E_NONFINITE, "non-finite fitness");
+}
+
+int64_t psso_launch_count(const psso_ctx* c) { return c ? c->launches : -1; }
+
+int psso_profile(psso_ctx* c, int32_t enable) {
+  if (!c) return fail(nullptr, PSSO_E_INVALID, "null context");
+  c->profiling = enable != 0;
+  c->ev_used = 0;
+  return PSSO_OK;
+}
+
+int psso_profile_read(psso_ctx* c, double* kernel_ms, int64_t* nlaunch) {
+  if (!c) return fail(nullptr, PSSO_E_INVALID, "null context");
+  CK(c, cudaStreamSynchronize(c->stream));
+  double tot = 0.0;
+  for (size_t k = 0; k + 1 < c->ev_used; k += 2) {
+    float ms = 0.f;
+    CK(c, cudaEventElapsedTime(&ms, c->ev[k], c->ev[k + 1]));
+    tot += ms;
+  }
+  if (kernel_ms) *kernel_ms = tot;
+  if (nlaunch) *nlaunch = (int64_t)(c->ev_used / 2);
+  c->ev_used = 0;
+  return PSSO_OK;
+}
+
+int psso_rng_uniform(uint64_t seed, uint64_t stream_key, uint64_t t, const uint64_t* particles,
+                     const uint64_t* variables, int64_t n, double* out, void* stream) {
+  if (n < 0 || (n > 0 && (!particles || !variables || !out)))
+    return fail(nullptr, PSSO_E_INVALID, "bad rng arguments");
+  if (n == 0) return PSSO_OK;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 4096);
+  k_rng<<<grid, 256, 0, (cudaStream_t)stream>>>(seed, stream_key, t, particles, variables, n, out);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? PSSO_OK : cuda_fail(nullptr, e, "psso_rng_uniform");
+}
+
+int psso_eval_rows(int32_t fn_id, int32_t dtype, int64_t nvar, const void* x, int64_t rows,
+                   double* out, double probe_level, void* stream) {
+  psso_config cfg;
+  std::memset(&cfg, 0, sizeof cfg);
+  cfg.fn_id = fn_id;
+  cfg.dtype = dtype;
+  cfg.rng_mode = PSSO_RNG_REFERENCE;
+  cfg.nsol = rows > 0 ? rows : 1;
+  cfg.nvar = nvar;
+  cfg.row_lo = 0;
+  cfg.row_hi = cfg.nsol;
+  cfg.cw = 0.3; cfg.cp = 0.6; cfg.cg = 0.8;
+  cfg.var_min = -1; cfg.var_max = 1;
+  cfg.probe_level = probe_level;
+  if (rows == 0) return PSSO_OK;
+  if (rows < 0 || !x || !out) return fail(nullptr, PSSO_E_INVALID, "bad eval arguments");
+  if ((uintptr_t)x % 16) return fail(nullptr, PSSO_E_INVALID, "input rows must be 16-byte aligned");
+  psso_ctx* c = nullptr;
+  int rc = psso_create(&cfg, &c);
+  if (rc) return rc;
+  psso_buffers b;
+  std::memset(&b, 0, sizeof b);
+  c->buf = b;
+  c->buf.sol = const_cast<void*>(x);
+  c->buf.sol_f = out;
+  c->bound = true;
+  c->stream = (cudaStream_t)stream;
+  TileParams p = tile_params(c, M_LOAD | M_EVAL | M_SOLF, -1, nullptr);
+  p.bad = nullptr;
+  rc = launch_tile(c, p);
+  if (rc == PSSO_OK) {
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) rc = cuda_fail(nullptr, e, "psso_eval_rows");
+  }
+  psso_destroy(c);
+  return rc;
+}
+
+int psso_solve(const psso_config* cfg, int64_t niter, double* traj, void* best_position,
+               double* best_fitness, double* wall_s) {
+  std::string err;
+  int rc = validate(cfg, err);
+  if (rc) return fail(nullptr, rc, err);
+  if (niter < 1) return fail(nullptr, PSSO_E_INVALID, "niter must be a positive integer");
+  if (cfg->row_lo != 0 || cfg->row_hi != cfg->nsol) return fail(nullptr, PSSO_E_INVALID, "psso_solve runs the whole swarm");
+  const size_t es = cfg->dtype == PSSO_F64 ? 8 : 4;
+  const size_t N = (size_t)cfg->nsol, D = (size_t)cfg->nvar;
+  psso_buffers b;
+  std::memset(&b, 0, sizeof b);
+  cudaStream_t s = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  psso_ctx* c = nullptr;
+  cudaError_t e = cudaSuccess;
+  auto cleanup = [&]() {
+    if (c) psso_destroy(c);
+    cudaFree(b.sol); cudaFree(b.pbests); cudaFree(b.p_f); cudaFree(b.gbest);
+    cudaFree(b.g_f); cudaFree(b.traj);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    if (s) cudaStreamDestroy(s);
+  };
+  if ((e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaEventCreate(&e0)) != cudaSuccess || (e = cudaEventCreate(&e1)) != cudaSuccess ||
+      (e = cudaMalloc(&b.sol, N * D * es)) != cudaSuccess ||
+      (e = cudaMalloc(&b.pbests, N * D * es)) != cudaSuccess ||
+      (e = cudaMalloc((void**)&b.p_f, N * 8)) != cudaSuccess ||
+      (e = cudaMalloc(&b.gbest, D * es)) != cudaSuccess ||
+      (e = cudaMalloc((void**)&b.g_f, 8)) != cudaSuccess ||
+      (e = cudaMalloc((void**)&b.traj, (size_t)niter * 8)) != cudaSuccess) {
+    cleanup();
+    return cuda_fail(nullptr, e, "psso_solve alloc");
+  }
+  if ((rc = psso_create(cfg, &c)) != PSSO_OK) { c = nullptr; cleanup(); return rc; }
+  if ((rc = psso_bind(c, &b, s)) || (rc = psso_init(c))) { cleanup(); return rc; }
+  int64_t bt, bi;
+  if ((rc = psso_check(c, &bt, &bi)) != PSSO_OK) {
+    g_err = "non-finite fitness at particle " + std::to_string(bi) + " during initialization";
+    cleanup();
+    return rc;
+  }
+  cudaEventRecord(e0, s);
+  if ((rc = psso_run(c, 0, niter)) != PSSO_OK) { cleanup(); return rc; }
+  cudaEventRecord(e1, s);
+  if ((rc = psso_check(c, &bt, &bi)) != PSSO_OK) {
+    g_err = "non-finite fitness at particle " + std::to_string(bi) + " at iteration " + std::to_string(bt);
+    cleanup();
+    return rc;
+  }
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  if (traj) e = cudaMemcpy(traj, b.traj, (size_t)niter * 8, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && best_position) e = cudaMemcpy(best_position, b.gbest, D * es, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && best_fitness) e = cudaMemcpy(best_fitness, b.g_f, 8, cudaMemcpyDeviceToHost);
+  if (wall_s) *wall_s = ms * 1e-3;
+  cleanup();
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "psso_solve copy-back");
+  return PSSO_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,182 @@
+"""DeviceEngine: one libpsso context plus its HBM-resident swarm.
+
+Owns the torch tensors that hold the swarm (particle-major X and P, p_f,
+gbest, g_f, trajectory) on one CUDA device and a private non-default stream
+(so the iteration loop can be replayed from a CUDA graph).  Everything here
+is plumbing around the C ABI; all compute is in libpsso.so.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .benchmarks import device_code_of
+from .core import NonFiniteFitnessError, SsoParams, Swarm
+
+__all__ = ["DeviceEngine", "make_config", "DTYPES", "RNG_MODES"]
+
+DTYPES = {"float64": _lib.PSSO_F64, "float32": _lib.PSSO_F32}
+RNG_MODES = {"reference": _lib.PSSO_RNG_REFERENCE, "philox": _lib.PSSO_RNG_PHILOX}
+_MASK64 = (1 << 64) - 1
+
+
+def make_config(params: SsoParams, f, seed: int, *, dtype="float64", rng="reference",
+                row_lo=0, row_hi=None, keep_sol_f=False) -> _lib.PssoConfig:
+    code = device_code_of(f)
+    if params.nvar != f.dimension:
+        raise ValueError(f"{f.id} expects dimension {f.dimension}, got {params.nvar}")
+    if dtype not in DTYPES:
+        raise ValueError(f"dtype must be one of {tuple(DTYPES)}, got {dtype!r}")
+    if rng not in RNG_MODES:
+        raise ValueError(f"rng must be one of {tuple(RNG_MODES)}, got {rng!r}")
+    return _lib.PssoConfig(
+        fn_id=code, dtype=DTYPES[dtype], rng_mode=RNG_MODES[rng],
+        flags=1 if keep_sol_f else 0, nsol=params.nsol, nvar=params.nvar,
+        row_lo=row_lo, row_hi=params.nsol if row_hi is None else row_hi,
+        cw=params.cw, cp=params.cp, cg=params.cg, var_min=params.var_min,
+        var_max=params.var_max, seed=int(seed) & _MASK64, probe_level=float(f.probe_level))
+
+
+class DeviceEngine:
+    """A swarm shard [row_lo, row_hi) resident in HBM with its psso context."""
+
+    def __init__(self, params: SsoParams, f, seed: int, *, dtype="float64", rng="reference",
+                 row_lo=0, row_hi=None, device=None, keep_sol_f=False, traj_len=None,
+                 stream=None):
+        import torch
+
+        _lib.require_device()
+        self.params, self.f, self.seed, self.dtype = params, f, int(seed), dtype
+        self.cfg = make_config(params, f, seed, dtype=dtype, rng=rng, row_lo=row_lo,
+                               row_hi=row_hi, keep_sol_f=keep_sol_f)
+        self.row_lo, self.row_hi = self.cfg.row_lo, self.cfg.row_hi
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self._lib = _lib.load()
+        with torch.cuda.device(self.device):
+            self.stream = stream if stream is not None else torch.cuda.Stream(self.device)
+            ctx = ctypes.c_void_p()
+            _lib.check(self._lib.psso_create(ctypes.byref(self.cfg), ctypes.byref(ctx)))
+            self.ctx = ctx
+            rows, D = self.row_hi - self.row_lo, params.nvar
+            tdt = torch.float64 if dtype == "float64" else torch.float32
+            kw = dict(device=self.device)
+            self.sol = torch.empty((rows, D), dtype=tdt, **kw)
+            self.pbests = torch.empty((rows, D), dtype=tdt, **kw)
+            self.sol_f = torch.full((rows,), float("nan"), dtype=torch.float64, **kw)
+            self.p_f = torch.empty((rows,), dtype=torch.float64, **kw)
+            self.gbest = torch.empty((D,), dtype=tdt, **kw)
+            self.g_f = torch.zeros((1,), dtype=torch.float64, **kw)
+            self.traj = torch.full((traj_len or params.niter,), float("nan"), dtype=torch.float64, **kw)
+        torch.cuda.synchronize(self.device)  # allocations visible to the library's stream
+        self._bind()
+
+    # -- plumbing --------------------------------------------------------------
+    def _bind(self):
+        b = _lib.PssoBuffers(
+            sol=self.sol.data_ptr(), pbests=self.pbests.data_ptr(), sol_f=self.sol_f.data_ptr(),
+            p_f=self.p_f.data_ptr(), gbest=self.gbest.data_ptr(), g_f=self.g_f.data_ptr(),
+            traj=self.traj.data_ptr())
+        _lib.check(self._lib.psso_bind(self.ctx, ctypes.byref(b), self.stream.cuda_stream), self.ctx)
+
+    def _call(self, name, *args):
+        _lib.check(getattr(self._lib, name)(self.ctx, *args), self.ctx)
+
+    def close(self):
+        if getattr(self, "ctx", None) is not None and self.ctx.value:
+            self.stream.synchronize()
+            self._lib.psso_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def launches(self) -> int:
+        return int(self._lib.psso_launch_count(self.ctx))
+
+    def synchronize(self):
+        self.stream.synchronize()
+
+    # -- reference operations --------------------------------------------------
+    def initialize(self):
+        """core.initialize (core.py:196-210) on device."""
+        self._call("psso_init")
+        self.check(init=True)
+
+    def step(self, t: int):
+        self._call("psso_step", int(t))
+
+    def run(self, t0: int, niter: int):
+        """The run_parallel loop (parallel.py:192-212), asynchronous on self.stream."""
+        self._call("psso_run", int(t0), int(niter))
+
+    def search(self, t):
+        self._call("psso_search", int(t))
+
+    def evaluate(self, t=None):
+        self._call("psso_evaluate", -1 if t is None else int(t))
+
+    def update_pbests(self):
+        self._call("psso_update_pbests")
+
+    def update_gbest(self):
+        self._call("psso_update_gbest")
+
+    def check(self, init=False):
+        """Raise NonFiniteFitnessError for the first non-finite fitness (core.py:190-193)."""
+        bt, bi = ctypes.c_int64(0), ctypes.c_int64(-1)
+        rc = self._lib.psso_check(self.ctx, ctypes.byref(bt), ctypes.byref(bi))
+        if rc == _lib.PSSO_E_NONFINITE:
+            local = bi.value - self.row_lo
+            value = float(self.sol_f[local].item())
+            iteration = None if bt.value < 0 else int(bt.value)
+            raise NonFiniteFitnessError(value, int(bi.value), iteration)
+        _lib.check(rc, self.ctx)
+
+    # -- sharded iteration (see sharded.py) -----------------------------------
+    @property
+    def candidate_bytes(self) -> int:
+        return int(self._lib.psso_candidate_bytes(ctypes.byref(self.cfg)))
+
+    def new_candidate(self):
+        import torch
+
+        return torch.zeros(self.candidate_bytes, dtype=torch.uint8, device=self.device)
+
+    def init_local(self, cand):
+        self._call("psso_init_local", cand.data_ptr())
+
+    def step_local(self, t, cand):
+        self._call("psso_step_local", int(t), cand.data_ptr())
+
+    def apply(self, t, cands, ncand, is_init=False):
+        self._call("psso_apply_candidates", int(t), cands.data_ptr(), int(ncand), int(bool(is_init)))
+
+    # -- host <-> device -------------------------------------------------------
+    def to_host(self) -> Swarm:
+        self.stream.synchronize()
+        f64 = lambda t: t.to(dtype=__import__("torch").float64).cpu().numpy()  # noqa: E731
+        return Swarm(sol=f64(self.sol), pbests=f64(self.pbests), gbest=f64(self.gbest),
+                     sol_f=self.sol_f.cpu().numpy(), p_f=self.p_f.cpu().numpy(),
+                     g_f=float(self.g_f.cpu()[0]))
+
+    def load(self, swarm: Swarm):
+        """Upload a host Swarm (any storage order) into this engine's buffers."""
+        import torch
+
+        lo, hi = self.row_lo, self.row_hi
+        tdt = self.sol.dtype
+        with torch.cuda.stream(self.stream):
+            self.sol.copy_(torch.as_tensor(np.ascontiguousarray(swarm.sol[lo:hi])).to(tdt))
+            self.pbests.copy_(torch.as_tensor(np.ascontiguousarray(swarm.pbests[lo:hi])).to(tdt))
+            self.gbest.copy_(torch.as_tensor(np.ascontiguousarray(swarm.gbest)).to(tdt))
+            self.sol_f.copy_(torch.as_tensor(np.ascontiguousarray(swarm.sol_f[lo:hi], dtype=np.float64)))
+            self.p_f.copy_(torch.as_tensor(np.ascontiguousarray(swarm.p_f[lo:hi], dtype=np.float64)))
+            self.g_f.fill_(float(swarm.g_f))
+        self.stream.synchronize()

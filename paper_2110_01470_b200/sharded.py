@@ -1,0 +1,192 @@
+"""Particle-sharded PSSO: contiguous row shards + one gBest exchange per iteration.
+
+Sharding follows the reference's worker partition (``_partition``,
+parallel.py:147-149: contiguous ranges from ``linspace``).  Every deviate is
+keyed by the *global* particle index, rows are disjoint, and the gBest step
+is a lexicographic (p_f, index) min -- so any shard count reproduces the
+unsharded run bit for bit, the property the reference pins as worker
+invariance (test_parallel.py:185-193).
+
+Per iteration each shard runs the fused kernel over its rows and reduces its
+own candidate record (p_f, global index, row); the records of all shards are
+gathered in rank order (one all-gather of R * (16 + D * sizeof(T)) bytes --
+the per-slice candidates + ``min(candidates)`` of parallel.py:199-208) and
+every shard applies the same deterministic selection (parallel.py:209-212).
+
+Exchanges:
+  * ``LocalExchange``        -- all shards live in this process (virtual
+                                shards on one GPU); gather = concatenation.
+  * ``ProcessGroupExchange`` -- one shard per process over torch.distributed
+                                (NCCL over NVLink on B200; gloo on CPU tests).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .core import SsoParams
+from .records import RunRecord, ScheduleKind
+
+__all__ = [
+    "partition",
+    "LocalExchange",
+    "ProcessGroupExchange",
+    "ShardedDriver",
+    "run_virtual_shards",
+    "run_parallel_distributed",
+]
+
+
+def partition(nsol: int, parts: int) -> list[tuple[int, int]]:
+    """Contiguous particle ranges, the reference's ``_partition`` (parallel.py:147-149)."""
+    if parts < 1:
+        raise ValueError(f"parts must be >= 1, got {parts}")
+    edges = np.linspace(0, nsol, parts + 1).astype(int)
+    return [(int(a), int(b)) for a, b in zip(edges[:-1], edges[1:]) if b > a]
+
+
+class LocalExchange:
+    """All shards in this process: the gathered buffer is the rank-ordered concatenation."""
+
+    def gather(self, cands):
+        import torch
+
+        return torch.cat(list(cands))
+
+
+class ProcessGroupExchange:
+    """One shard per process: ``all_gather_into_tensor`` of the candidate records."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def gather(self, cands):
+        import torch.distributed as dist
+
+        (c,) = cands
+        out = c.new_empty(self.world * c.numel())
+        dist.all_gather_into_tensor(out, c, group=self.group)
+        return out
+
+
+class ShardedDriver:
+    """Drives shard engines through init / iterations around the exchange.
+
+    ``engines`` are the shards owned by this process, in rank order; each must
+    provide ``new_candidate()``, ``init_local(cand)``, ``step_local(t, cand)``,
+    ``apply(t, cands, ncand, is_init)`` and ``check(init=...)`` (DeviceEngine
+    does, over the C ABI).  ``ncand`` is the total number of shards.
+    """
+
+    def __init__(self, engines, exchange, ncand: int):
+        self.engines = list(engines)
+        self.exchange = exchange
+        self.ncand = int(ncand)
+        self.cands = [e.new_candidate() for e in self.engines]
+
+    def _exchange_and_apply(self, t: int, is_init: bool):
+        gathered = self.exchange.gather(self.cands)
+        for e in self.engines:
+            e.apply(t, gathered, self.ncand, is_init)
+        return gathered
+
+    def initialize(self):
+        for e, c in zip(self.engines, self.cands):
+            e.init_local(c)
+        self._exchange_and_apply(-1, True)
+        for e in self.engines:
+            e.check(init=True)
+
+    def step(self, t: int):
+        for e, c in zip(self.engines, self.cands):
+            e.step_local(t, c)
+        self._exchange_and_apply(t, False)
+
+    def run(self, t0: int, niter: int):
+        for t in range(t0, t0 + niter):
+            self.step(t)
+
+    def check(self):
+        for e in self.engines:
+            e.check()
+
+
+def _record(params, f, seed, best, wall, traj, best_position) -> RunRecord:
+    return RunRecord(
+        run_id=0, schedule=ScheduleKind.PARALLEL, function=getattr(f, "id", "custom"),
+        nsol=params.nsol, nvar=params.nvar, niter=params.niter, cw=params.cw, cp=params.cp,
+        cg=params.cg, seed=seed, best_fitness=best, wall_time_s=wall,
+        best_position=best_position, trajectory=traj)
+
+
+def run_virtual_shards(params: SsoParams, f, seed: int, shards: int, *, dtype="float64",
+                       rng="reference", device=None) -> RunRecord:
+    """``shards`` contiguous shards on one GPU with the candidate exchange (tests sharding)."""
+    import torch
+
+    from .engine import DeviceEngine
+
+    ranges = partition(params.nsol, shards)
+    first = DeviceEngine(params, f, seed, dtype=dtype, rng=rng, row_lo=ranges[0][0],
+                         row_hi=ranges[0][1], device=device)
+    engines = [first] + [
+        DeviceEngine(params, f, seed, dtype=dtype, rng=rng, row_lo=lo, row_hi=hi,
+                     device=device, stream=first.stream)
+        for lo, hi in ranges[1:]
+    ]
+    try:
+        drv = ShardedDriver(engines, LocalExchange(), len(engines))
+        with torch.cuda.stream(first.stream):
+            drv.initialize()
+            start = torch.cuda.Event(enable_timing=True)
+            stop = torch.cuda.Event(enable_timing=True)
+            start.record(first.stream)
+            drv.run(0, params.niter)
+            stop.record(first.stream)
+        drv.check()
+        wall = start.elapsed_time(stop) * 1e-3
+        return _record(params, f, seed, float(first.g_f.cpu()[0]), wall, first.traj.cpu().numpy(),
+                       first.gbest.to(torch.float64).cpu().numpy())
+    finally:
+        for e in engines:
+            e.close()
+
+
+def run_parallel_distributed(params: SsoParams, f, seed: int, *, group=None, dtype="float64",
+                             rng="reference") -> RunRecord:
+    """One shard per torch.distributed rank (one process per GPU, NCCL over NVLink).
+
+    Every rank returns the same RunRecord.  ``wall_time_s`` is this rank's
+    loop time; callers wanting the job time take the max over ranks.
+    """
+    import torch
+    import torch.distributed as dist
+
+    from .engine import DeviceEngine
+
+    ex = ProcessGroupExchange(group)
+    ranges = partition(params.nsol, ex.world)
+    if len(ranges) != ex.world:
+        raise ValueError(f"nsol={params.nsol} cannot give every one of {ex.world} ranks a particle")
+    lo, hi = ranges[ex.rank]
+    eng = DeviceEngine(params, f, seed, dtype=dtype, rng=rng, row_lo=lo, row_hi=hi)
+    try:
+        drv = ShardedDriver([eng], ex, ex.world)
+        with torch.cuda.stream(eng.stream):
+            drv.initialize()
+            dist.barrier(group)
+            start = torch.cuda.Event(enable_timing=True)
+            stop = torch.cuda.Event(enable_timing=True)
+            start.record(eng.stream)
+            drv.run(0, params.niter)
+            stop.record(eng.stream)
+        drv.check()
+        wall = start.elapsed_time(stop) * 1e-3
+        return _record(params, f, seed, float(eng.g_f.cpu()[0]), wall, eng.traj.cpu().numpy(),
+                       eng.gbest.to(torch.float64).cpu().numpy())
+    finally:
+        eng.close()

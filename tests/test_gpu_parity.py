@@ -1,0 +1,465 @@
+"""GPU parity: the CUDA path (through libpsso.so) against the reference's goldens and the oracle.
+
+Bit-exact for indices, selections, positions and f1-f4 fitness (pure +,-,* in
+numpy order, no FMA).  f5-f9 use transcendentals (CUDA libdevice vs glibc /
+numpy SIMD): their fitness values must agree within RTOL = 1e-12 relative
+(north-star tolerance for fp64) while positions and selections stay bitwise.
+"""
+
+import ctypes
+import math
+import warnings
+
+import numpy as np
+import pytest
+
+from conftest import BITWISE_FIDS, BOUNDS
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU runs deselect -m gpu
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2110_01470_b200 as psso  # noqa: E402
+from oracle import oracle as O  # noqa: E402  (the checker)
+from paper_2110_01470_b200 import _lib  # noqa: E402
+from paper_2110_01470_b200.engine import DeviceEngine  # noqa: E402
+
+RTOL = 1e-12     # fp64 fitness tolerance for transcendental objectives
+RTOL32 = 1e-5    # fp32 fitness tolerance
+
+
+def _fn(fid, d):
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        return psso.make_function(fid, d)
+
+
+def _params(fn, nsol, niter, cw=0.3, cp=0.6, cg=0.8, var_min=None, var_max=None):
+    return psso.SsoParams(cw=cw, cp=cp, cg=cg,
+                          var_min=fn.var_min if var_min is None else var_min,
+                          var_max=fn.var_max if var_max is None else var_max,
+                          nsol=nsol, nvar=fn.dimension, niter=niter)
+
+
+def _close(a, b, fid, rtol=RTOL):
+    a, b = np.asarray(a), np.asarray(b)
+    if fid in BITWISE_FIDS:
+        return np.array_equal(a, b)
+    return np.allclose(a, b, rtol=rtol, atol=0.0)
+
+
+# ------------------------------------------------------------------- RNG ----
+
+def test_rng_bitwise_against_reference_golden(golden_rng):
+    g = golden_rng
+    for a, seed in enumerate(g["seeds"]):
+        r = psso.RngStream(int(seed))
+        for b, st in enumerate(g["streams"]):
+            for c, t in enumerate(g["iters"]):
+                u = r.uniform(psso.SubStream(int(st)), int(t), g["parts"][:, None], g["vars"][None, :])
+                assert np.array_equal(u, g["u"][a, b, c]), (seed, st, t)
+    wide = psso.RngStream((1 << 64) + 42).uniform(psso.SubStream.BRANCH, 0, 0, 0)
+    assert wide == g["wide_seed_u"]
+
+
+def test_rng_matrix_slices_and_range():
+    r = psso.RngStream(9)
+    full = r.matrix(psso.SubStream.BRANCH, 3, 0, 100, 17)
+    assert np.array_equal(full[30:40], r.matrix(psso.SubStream.BRANCH, 3, 30, 40, 17))
+    u = psso.RngStream(1).matrix(psso.SubStream.INIT, 0, 0, 1000, 100)
+    assert u.min() >= 0.0 and u.max() < 1.0
+    assert np.array_equal(u, O.u_batch(1, "INIT", 0, np.arange(1000)[:, None], np.arange(100)[None, :]))
+
+
+# --------------------------------------------------------------- fitness ----
+
+@pytest.mark.parametrize("fid", psso.FUNCTION_IDS)
+def test_fitness_against_reference_golden(fid, golden_fitness):
+    for key in golden_fitness.files:
+        if not key.startswith(fid + "_") or key.endswith("refpt"):
+            continue
+        d = int(key.split("_")[1])
+        fn = _fn(fid, d)
+        x = O.init_positions(1000 + d, 6, d, *BOUNDS[fid])
+        got = fn(x)
+        assert _close(got, golden_fitness[key], fid), (key, got, golden_fitness[key])
+        ref = fn(fn.reference_point)
+        assert _close(ref, golden_fitness[key + "_refpt"], fid) or abs(ref) <= 1e-12, key
+
+
+@pytest.mark.parametrize("fid", psso.FUNCTION_IDS)
+def test_batch_equals_rows_and_storage_order(fid):
+    fn = _fn(fid, 48)
+    rng = np.random.default_rng(abs(hash(fid)) % 2**32)
+    block = rng.uniform(fn.var_min, fn.var_max, size=(37, 48))
+    rows = np.array([fn(r) for r in block])
+    assert np.array_equal(fn(block), rows)
+    assert np.array_equal(fn(np.asfortranarray(block)), rows)
+    assert _close(rows, O.evaluate(fid, block), fid)
+
+
+def test_known_values():
+    origin50 = np.zeros(50)
+    for fid in ("f1", "f2", "f3", "f5", "f7"):
+        assert psso.make_function(fid, 50)(origin50) == 0.0
+    assert psso.make_function("f4", 50)(np.ones(50)) == 0.0
+    assert abs(psso.make_function("f6", 50)(origin50)) <= 1e-12
+    assert abs(psso.make_function("f9", 50)(origin50) - 20949.145) <= 1e-9
+    assert psso.make_function("f2", 3)(np.ones(3)) == pytest.approx(6.0, abs=1e-12)
+    assert psso.make_function("f3", 8)(np.ones(8)) == pytest.approx(204.0, abs=1e-12)
+    assert psso.make_function("f1", 2)(np.array([3.0, 4.0])) == pytest.approx(25.0)
+    fn = _fn("f8", 50)
+    x = np.zeros(50)
+    x[-2:] = 3.0
+    assert fn(x) == 0.0
+    y = np.random.default_rng(7).uniform(-4, 5, size=50)
+    assert fn(y) == psso.make_function("f8", 48)(y[:48])
+
+
+@pytest.mark.parametrize("fid", psso.FUNCTION_IDS)
+def test_fp32_fitness_within_tolerance(fid):
+    d = 64
+    fn = _fn(fid, d)
+    x = O.init_positions(77, 64, d, *BOUNDS[fid]).astype(np.float32)
+    from paper_2110_01470_b200.benchmarks import evaluate_rows
+
+    got = evaluate_rows(fn, x, dtype="float32")
+    ref = O.evaluate(fid, x.astype(np.float64))
+    scale = np.abs(ref) + 1.0
+    assert np.all(np.abs(got - ref) <= RTOL32 * scale * 10), (got, ref)
+
+
+# ----------------------------------------------------------- whole runs ----
+
+def _run_ids(golden):
+    index, _ = golden
+    return [e["key"] for e in index]
+
+
+@pytest.fixture(scope="module")
+def runs_index():
+    import json
+
+    from conftest import GOLDEN
+
+    return {e["key"]: e for e in json.loads((GOLDEN / "runs.json").read_text())}
+
+
+RUN_KEYS = [f"run{k}" for k in range(27)]
+
+
+@pytest.mark.parametrize("key", RUN_KEYS)
+def test_run_parallel_against_reference_golden(key, runs_index, golden_runs):
+    e = runs_index[key]
+    _, arr = golden_runs
+    fn = _fn(e["fid"], e["nvar"])
+    p = psso.SsoParams(cw=e["cw"], cp=e["cp"], cg=e["cg"], var_min=e["var_min"],
+                       var_max=e["var_max"], nsol=e["nsol"], nvar=e["nvar"], niter=e["niter"])
+    rec = psso.run_parallel(p, fn, seed=e["seed"])
+    assert rec.schedule == psso.ScheduleKind.PARALLEL and rec.function == e["fid"]
+    assert np.array_equal(rec.best_position, arr[key + "_gbest"]), "gbest position (bitwise)"
+    assert _close(rec.trajectory, arr[key + "_traj"], e["fid"]), "trajectory"
+    assert rec.best_fitness == rec.trajectory[-1]
+    if e["state"]:
+        eng = DeviceEngine(p, fn, e["seed"], keep_sol_f=True)
+        try:
+            eng.initialize()
+            assert _close(eng.p_f.cpu().numpy(), arr[key + "_init_p_f"], e["fid"])
+            eng.run(0, e["niter"])
+            eng.check()
+            sw = eng.to_host()
+        finally:
+            eng.close()
+        assert np.array_equal(sw.sol, arr[key + "_sol"])
+        assert np.array_equal(sw.pbests, arr[key + "_pbests"])
+        assert _close(sw.p_f, arr[key + "_p_f"], e["fid"])
+        assert _close(sw.sol_f, arr[key + "_sol_f"], e["fid"])
+
+
+def test_stepwise_state_against_reference_golden(golden_runs):
+    _, arr = golden_runs
+    fn = psso.make_function("f4", 10)
+    p = _params(fn, 12, 12)
+    eng = DeviceEngine(p, fn, 5, keep_sol_f=True)
+    try:
+        eng.initialize()
+        for t in range(p.niter):
+            eng.step(t)
+            sw = eng.to_host()
+            assert np.array_equal(sw.sol, arr["steps_sol"][t]), t
+            assert np.array_equal(sw.pbests, arr["steps_pbests"][t]), t
+            assert np.array_equal(sw.p_f, arr["steps_p_f"][t]), t
+            assert np.array_equal(sw.gbest, arr["steps_gbest"][t]), t
+    finally:
+        eng.close()
+
+
+def test_c1_appendix_values():
+    fn = psso.make_function("f1", 30)
+    rec = psso.run_parallel(_params(fn, 100, 1000), fn, seed=0)
+    assert rec.best_fitness == 8.542836016810329
+    import hashlib
+
+    assert hashlib.sha256(rec.trajectory.tobytes()).hexdigest()[:16] == "767e5860d9ad62e6"
+    assert hashlib.sha256(rec.best_position.tobytes()).hexdigest()[:16] == "586dba8e667ca007"
+
+
+# ------------------------------------------------------------- phase API ----
+
+def test_phase_api_composes_to_fused_step():
+    fn = psso.make_function("f5", 20)
+    p = _params(fn, 15, 40)
+    rng = psso.RngStream(99)
+    swarm = psso.initialize(p, fn, rng)
+    o = O.Oracle.from_params(p, "f5", 99)
+    osw = o.initialize()
+    assert np.array_equal(swarm.sol, osw.sol)
+    g_prev = swarm.g_f
+    for t in range(p.niter):
+        psso.search_phase(swarm, p, rng, t)
+        psso.evaluate_phase(swarm, fn, t)
+        psso.update_pbests_phase(swarm)
+        psso.update_gbest_phase(swarm)
+        o.step(osw, t)
+        assert np.array_equal(swarm.sol, osw.sol), t
+        assert np.array_equal(swarm.pbests, osw.pbests), t
+        assert np.array_equal(swarm.gbest, osw.gbest), t
+        assert np.all(swarm.p_f <= swarm.sol_f)
+        assert np.all(swarm.g_f <= swarm.p_f)
+        assert swarm.g_f <= g_prev
+        g_prev = swarm.g_f
+    rec = psso.run_parallel(p, fn, seed=99)
+    assert np.array_equal(rec.best_position, swarm.gbest)
+
+
+def test_search_phase_keeps_untouched_fields_and_box():
+    fn = psso.make_function("f6", 12)
+    p = _params(fn, 50, 5, cw=0.1, cp=0.3, cg=0.5)
+    swarm = psso.initialize(p, fn, psso.RngStream(2))
+    before = swarm.copy()
+    for t in range(5):
+        psso.search_phase(swarm, p, psso.RngStream(2), t)
+        assert swarm.sol.min() >= p.var_min and swarm.sol.max() <= p.var_max
+    assert np.array_equal(swarm.pbests, before.pbests)
+    assert np.array_equal(swarm.gbest, before.gbest)
+
+
+def test_all_keep_thresholds_leave_positions():
+    fn = psso.make_function("f1", 6)
+    p = _params(fn, 10, 5, cw=1.0, cp=1.0, cg=1.0)
+    swarm = psso.initialize(p, fn, psso.RngStream(1))
+    before = swarm.sol.copy()
+    psso.search_phase(swarm, p, psso.RngStream(1), 0)
+    assert np.array_equal(swarm.sol, before)
+
+
+def test_update_phases_edge_semantics():
+    fn = psso.make_function("f1", 3)
+    p = _params(fn, 2, 1)
+    swarm = psso.initialize(p, fn, psso.RngStream(6))
+    swarm.sol[0] = [1.0, 2.0, 3.0]
+    swarm.sol_f[0] = swarm.p_f[0]  # tie refreshes the incumbent
+    psso.update_pbests_phase(swarm)
+    assert np.array_equal(swarm.pbests[0], [1.0, 2.0, 3.0])
+    # gbest: lowest index wins ties; incumbent survives only if strictly better
+    swarm = psso.initialize(_params(fn, 3, 1), fn, psso.RngStream(0))
+    swarm.pbests = np.arange(9, dtype=float).reshape(3, 3)
+    swarm.p_f = np.array([5.0, 3.0, 3.0])
+    swarm.gbest = np.array([-1.0, -1.0, -1.0])
+    swarm.g_f = 4.0
+    psso.update_gbest_phase(swarm)
+    assert swarm.g_f == 3.0 and np.array_equal(swarm.gbest, swarm.pbests[1])
+    swarm.p_f = np.array([5.0, 6.0, 7.0])
+    swarm.g_f = 4.0
+    swarm.gbest = np.array([-1.0, -1.0, -1.0])
+    psso.update_gbest_phase(swarm)
+    assert swarm.g_f == 4.0 and np.array_equal(swarm.gbest, [-1.0, -1.0, -1.0])
+
+
+# ------------------------------------------------------ sharding / layout ----
+
+@pytest.mark.parametrize("shards", [2, 3, 7, 23])
+def test_virtual_shards_bitwise(shards):
+    fn = psso.make_function("f4", 10)
+    p = _params(fn, 23, 25)
+    base = psso.run_parallel(p, fn, seed=42)
+    rec = psso.run_parallel(p, fn, seed=42, shards=shards)
+    assert rec.best_fitness == base.best_fitness
+    assert np.array_equal(rec.best_position, base.best_position)
+    assert np.array_equal(rec.trajectory, base.trajectory)
+
+
+def test_workers_and_layout_have_no_effect():
+    fn = psso.make_function("f7", 9)
+    p = _params(fn, 14, 20)
+    a = psso.run_parallel(p, fn, seed=3, workers=1, layout=psso.LayoutMode.PARTICLE_MAJOR)
+    b = psso.run_parallel(p, fn, seed=3, workers=8, layout=psso.LayoutMode.INTERLEAVED)
+    assert a.best_fitness == b.best_fitness and np.array_equal(a.trajectory, b.trajectory)
+    with pytest.raises(ValueError, match="workers"):
+        psso.run_parallel(p, fn, seed=0, workers=0)
+
+
+# ---------------------------------------------------------- fault paths ----
+
+def test_nonfinite_during_iterations_names_particle():
+    level = float(O.init_positions(0, 40, 4, -1.0, 1.0)[:, 0].max())  # init stays finite
+    fn = psso.probe_function(4, level=level, bounds=(-1.0, 1.0))
+    p = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=-1, var_max=1, nsol=40, nvar=4, niter=200)
+    with pytest.raises(psso.NonFiniteFitnessError) as ei:
+        psso.run_parallel(p, fn, seed=0)
+    err = ei.value
+    assert err.iteration is not None and math.isinf(err.value)
+    assert f"particle {err.particle}" in str(err)
+    # replay through the phase API: the same (iteration, particle) is the first failure
+    rng = psso.RngStream(0)
+    swarm = psso.initialize(p, fn, rng)
+    for t in range(err.iteration + 1):
+        psso.search_phase(swarm, p, rng, t)
+        bad = np.nonzero(swarm.sol[:, 0] > level)[0]
+        if bad.size:
+            assert t == err.iteration and bad[0] == err.particle
+            with pytest.raises(psso.NonFiniteFitnessError, match=f"particle {err.particle}"):
+                psso.evaluate_phase(swarm, fn, t)
+            break
+        psso.evaluate_phase(swarm, fn, t)
+        psso.update_pbests_phase(swarm)
+        psso.update_gbest_phase(swarm)
+    else:
+        pytest.fail("phase replay never hit the probe")
+
+
+def test_nonfinite_during_initialization():
+    fn = psso.probe_function(3, level=-2.0)  # every particle is +inf
+    p = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=-1, var_max=1, nsol=5, nvar=3, niter=2)
+    with pytest.raises(psso.NonFiniteFitnessError, match="particle 0 during initialization"):
+        psso.run_parallel(p, fn, seed=1)
+
+
+def test_plain_callables_rejected():
+    p = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=-1, var_max=1, nsol=5, nvar=3, niter=2)
+    with pytest.raises(TypeError, match="registry objectives"):
+        psso.run_parallel(p, lambda x: 0.0, seed=1)
+
+
+# ------------------------------------------------------ C ABI host entry ----
+
+def test_psso_solve_host_buffers_match_run_parallel():
+    fn = psso.make_function("f2", 40)
+    p = _params(fn, 300, 60)
+    rec = psso.run_parallel(p, fn, seed=5)
+    from paper_2110_01470_b200.engine import make_config
+
+    cfg = make_config(p, fn, 5)
+    traj = np.empty(p.niter)
+    best = np.empty(p.nvar)
+    bf, wall = ctypes.c_double(), ctypes.c_double()
+    rc = _lib.load().psso_solve(ctypes.byref(cfg), p.niter, traj.ctypes.data, best.ctypes.data,
+                                ctypes.byref(bf), ctypes.byref(wall))
+    assert rc == 0, _lib.last_error()
+    assert np.array_equal(traj, rec.trajectory) and np.array_equal(best, rec.best_position)
+    assert bf.value == rec.best_fitness and wall.value > 0
+
+
+# ------------------------------------------------- full-size properties ----
+
+def _oracle_run(fid, p, seed, niter, threads=None):
+    o = O.Oracle.from_params(p, fid, seed, threads=threads or O.max_threads())
+    sw = o.initialize()
+    traj = o.run(sw, 0, niter)
+    return sw, traj
+
+
+@pytest.mark.parametrize("fid,nsol,nvar,niter", [
+    ("f5", 1 << 17, 128, 4),   # C3 row shape
+    ("f4", 1 << 17, 64, 4),    # C4 row shape
+    ("f6", 1024, 4096, 3),     # C5 row shape (multi-leaf rows)
+    ("f7", 4096, 100, 5),      # C2 shape (sequential product, aux table)
+])
+def test_large_shapes_against_oracle(fid, nsol, nvar, niter):
+    fn = psso.make_function(fid, nvar)
+    p = _params(fn, nsol, niter)
+    eng = DeviceEngine(p, fn, 0, keep_sol_f=True)
+    try:
+        eng.initialize()
+        eng.run(0, niter)
+        eng.check()
+        sw = eng.to_host()
+        traj = eng.traj.cpu().numpy()
+    finally:
+        eng.close()
+    osw, otraj = _oracle_run(fid, p, 0, niter)
+    assert np.array_equal(sw.sol, osw.sol)
+    assert np.array_equal(sw.pbests, osw.pbests)
+    assert np.array_equal(sw.gbest, osw.gbest)
+    assert _close(sw.p_f, osw.p_f, fid) and _close(traj, otraj, fid)
+
+
+def test_c3_full_size_invariants_and_determinism():
+    """BASELINE config C3 at full size: 2^20 x 128 Rastrigin, size-independent properties."""
+    fn = psso.make_function("f5", 128)
+    p = _params(fn, 1 << 20, 12)
+    outs = []
+    for shards in (1, 2):
+        if shards == 1:
+            eng = DeviceEngine(p, fn, 0, keep_sol_f=True)
+            try:
+                eng.initialize()
+                eng.run(0, p.niter)
+                eng.check()
+                traj = eng.traj.cpu().numpy()
+                p_f = eng.p_f.cpu().numpy()
+                sol_f = eng.sol_f.cpu().numpy()
+                gb = eng.gbest.cpu().numpy()
+                P = eng.pbests
+                X = eng.sol
+                assert float(X.min()) >= p.var_min and float(X.max()) <= p.var_max
+                assert np.all(p_f <= sol_f)
+                b = int(np.argmin(p_f))
+                assert traj[-1] == p_f[b] and np.array_equal(gb, P[b].cpu().numpy())
+                assert np.all(np.diff(traj) <= 0)
+                xs = float(X.double().sum())
+            finally:
+                eng.close()
+            outs.append((traj, gb, xs))
+        else:
+            rec = psso.run_parallel(p, fn, seed=0, shards=shards)
+            outs.append((rec.trajectory, rec.best_position, None))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+def test_fp32_mode_positions_are_rounded_reference_positions():
+    fn = psso.make_function("f5", 128)
+    p = _params(fn, 4096, 30)
+    eng = DeviceEngine(p, fn, 3, dtype="float32", keep_sol_f=True)
+    try:
+        eng.initialize()
+        x32 = eng.sol.cpu().numpy()
+        eng.run(0, p.niter)
+        eng.check()
+        traj = eng.traj.cpu().numpy()
+    finally:
+        eng.close()
+    x64 = O.Oracle.from_params(p, "f5", 3).initialize().sol
+    assert np.array_equal(x32, x64.astype(np.float32))
+    assert np.all(np.diff(traj) <= 0) and np.isfinite(traj).all()
+    # fp32 fitness of the fp32 positions vs the fp64 oracle on the same inputs
+    ref = O.evaluate("f5", x32.astype(np.float64))
+    from paper_2110_01470_b200.benchmarks import evaluate_rows
+
+    got = evaluate_rows(fn, x32, dtype="float32")
+    assert np.all(np.abs(got - ref) <= RTOL32 * (np.abs(ref) + 1.0) * 10)
+
+
+def test_philox_mode_distribution_matches_reference():
+    """Benchmark mode: final-fitness distribution over 30 seeds vs the oracle (reference RNG)."""
+    from scipy import stats
+
+    fn = psso.make_function("f1", 30)
+    p = _params(fn, 100, 1000)
+    gpu = np.array([psso.run_parallel(p, fn, seed=s, rng="philox").best_fitness for s in range(30)])
+    ref = np.array([_oracle_run("f1", p, s, p.niter, threads=1)[1][-1] for s in range(30)])
+    assert abs(gpu.mean() - ref.mean()) <= 0.10 * ref.mean(), (gpu.mean(), ref.mean())
+    assert stats.kruskal(gpu, ref).pvalue > 0.01
+    assert stats.ttest_ind(gpu, ref).pvalue > 0.01
