@@ -46,6 +46,9 @@ WORKLOADS = {
     "c4": ("f4", 1 << 24, 64, "float64", "C4 Rosenbrock N=2^24 Nvar=64 fp64"),
     "c5": ("f6", 65536, 4096, "float64", "C5 Ackley N=65536 Nvar=4096 fp64"),
     "c2": ("f5", 1024, 100, "float64", "C2 Rastrigin N=1024 Nvar=100 fp64"),
+    # diagnostics (not BASELINE configs): C3 shape with the cheapest objective
+    "c3sphere": ("f1", 1 << 20, 128, "float64", "diagnostic: Sphere N=2^20 Nvar=128 fp64"),
+    "c3sphere32": ("f1", 1 << 20, 128, "float32", "diagnostic: Sphere N=2^20 Nvar=128 fp32"),
 }
 
 
@@ -122,7 +125,8 @@ def cpu_baseline(fid, nvar, steps_budget_s=12.0, sample_rows=1 << 16, dtype="flo
     from oracle import oracle as O
 
     threads = O.max_threads()
-    lo, hi = {"f5": (-5.12, 5.12), "f4": (-2.048, 2.048), "f6": (-32.768, 32.768)}[fid]
+    lo, hi = {"f1": (-5.12, 5.12), "f5": (-5.12, 5.12), "f4": (-2.048, 2.048),
+              "f6": (-32.768, 32.768)}[fid]
     o = O.Oracle(fid, sample_rows, nvar, 0.3, 0.6, 0.8, lo, hi, 0, threads=threads)
     sw = o.initialize()
     o.run(sw, 0, 1)  # warm
@@ -147,7 +151,8 @@ def run_reference(args, wl):
 
     threads = O.max_threads()
     sample = min(nsol, 1 << 16) if nvar <= 256 else min(nsol, 1 << 11)
-    lo, hi = {"f5": (-5.12, 5.12), "f4": (-2.048, 2.048), "f6": (-32.768, 32.768)}[fid]
+    lo, hi = {"f1": (-5.12, 5.12), "f5": (-5.12, 5.12), "f4": (-2.048, 2.048),
+              "f6": (-32.768, 32.768)}[fid]
     o = O.Oracle(fid, sample, nvar, 0.3, 0.6, 0.8, lo, hi, 0, threads=threads)
     sw = o.initialize()
     o.run(sw, 0, args.warmup)
@@ -279,7 +284,7 @@ def run_ours(args, wl):
     if rank != 0:
         dist.destroy_process_group()
         return
-    cpu = cpu_baseline(fid, nvar) if ws == 1 else None
+    cpu = cpu_baseline(fid, nvar) if ws == 1 and not args.no_cpu else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -295,7 +300,7 @@ def run_ours(args, wl):
                                                              "candidates per iteration" if ws > 1 else "")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
-                     "kernel": "k_tile<%s,f5,ref>" % ("double" if es == 8 else "float"),
+                     "kernel": "k_tile<%s,%s,%s>" % ("double" if es == 8 else "float", fid, args.rng),
                      "kernel_ms": kern_ms, "alg_bytes_per_launch": alg_bytes,
                      "alg_bytes_per_pvu": 3 * es},
         "gpu_launches": launches,
@@ -316,6 +321,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--rng", default="reference", choices=["reference", "philox"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg (diagnostics)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -11,7 +11,7 @@ import ctypes
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libpsso.so"
+LIB_PATH = Path(os.environ.get("PSSO_LIB") or Path(__file__).resolve().parent / "libpsso.so")
 
 PSSO_OK = 0
 PSSO_E_INVALID = 1

@@ -6,6 +6,7 @@
 // parallel.py:152-233; phases parallel.py:120-144; initialize core.py:196-210;
 // RngStream.uniform rng.py:73-87; BenchmarkFn.__call__ benchmarks.py:86-94.
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -26,8 +27,10 @@ constexpr int GRAPH_CHUNK = 16;  // iterations per captured graph
 
 struct Layout {
   int V, R, G, S, NL;
+  bool pre;
   size_t smem;
-  int off_xs, off_scr, off_gb, off_hb, off_hf, off_leaf, off_rowf, off_flag, off_red;
+  int off_xs, off_scr, off_gb, off_hb, off_hf, off_leaf, off_rowf, off_flag, off_red, off_bar;
+  int stage_bytes;
   Plan plan;
 };
 
@@ -79,7 +82,12 @@ int64_t terms_of(int fn, int64_t D) {
 
 size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-bool make_layout(int fn, int dtype, int64_t D, Layout& L, std::string& err) {
+constexpr bool heavy_fn(int fn) { return fn == 5 || fn == 6 || fn == 8 || fn == 9; }
+
+// Shared-memory layout of a tile kernel.  k_tile (fused=false): padded xs
+// tile + optional term buffer.  k_fused (fused=true): two TMA stages of
+// contiguous X and P tiles + optional term buffer, sized for two CTAs per SM.
+bool make_layout(int fn, int dtype, int64_t D, bool fused, Layout& L, std::string& err) {
   const int es = dtype == PSSO_F64 ? 8 : 4;
   if (!build_plan(terms_of(fn, D), L.plan, err)) return false;
   L.NL = L.plan.nleaves;
@@ -89,29 +97,31 @@ bool make_layout(int fn, int dtype, int64_t D, Layout& L, std::string& err) {
   int64_t S = D;
   while (S % mod != 8 % mod || S % L.V) ++S;  // chain reads conflict-free
   L.S = (int)S;
-  const bool scr = (fn == 3 || fn == 7);
-  const size_t fixed = align16(D * es) + 128;
+  auto needs_buf = [&](int R) { return fn == 3 || fn == 7 || (heavy_fn(fn) && R * L.G < NT); };
   auto smem_for = [&](int R) {
-    size_t s = align16((size_t)R * S * es);        // xs
-    s += scr ? align16((size_t)R * S * 8) : 0;     // scratch
-    s += align16(D * es);                          // gbest
-    s += 2 * align16((size_t)R * 8);               // hashes
-    s += align16((size_t)R * L.NL * 16);           // leaf values
-    s += align16((size_t)R * 8) + align16((size_t)R * 4) + 128;
+    size_t s = fused ? 2 * align16((size_t)2 * R * D * es) : align16((size_t)R * S * es);
+    s += needs_buf(R) ? align16((size_t)R * S * es) : 0;  // term buffer
+    s += align16(D * es);                                  // gbest
+    s += 2 * align16((size_t)R * 8);                       // hashes
+    s += align16((size_t)R * L.NL * 16);                   // leaf values
+    s += align16((size_t)R * 8) + align16((size_t)R * 4) + 128 + 16;
     return s;
   };
-  (void)fixed;
-  int R = L.G >= NT ? 1 : NT / L.G;
-  const size_t cap = 200 * 1024;
+  int R = 1;
+  while (2 * R * L.G <= NT) R *= 2;  // chains of R rows fill at most one CTA
+  const size_t cap = fused ? 110 * 1024 : 200 * 1024;
   while (R > 1 && smem_for(R) > cap) R /= 2;
   if (smem_for(R) > 227 * 1024) {
     err = "nvar " + std::to_string(D) + " too large for the shared-memory row tile";
     return false;
   }
   L.R = R;
+  L.pre = heavy_fn(fn) && R * L.G < NT;
+  const bool buf = needs_buf(R);
   size_t o = 0;
-  L.off_xs = (int)o; o += align16((size_t)R * S * es);
-  L.off_scr = (int)o; o += scr ? align16((size_t)R * S * 8) : 0;
+  L.stage_bytes = (int)align16((size_t)2 * R * D * es);
+  L.off_xs = (int)o; o += fused ? 2 * (size_t)L.stage_bytes : align16((size_t)R * S * es);
+  L.off_scr = (int)o; o += buf ? align16((size_t)R * S * es) : 0;
   L.off_gb = (int)o; o += align16(D * es);
   L.off_hb = (int)o; o += align16((size_t)R * 8);
   L.off_hf = (int)o; o += align16((size_t)R * 8);
@@ -119,6 +129,7 @@ bool make_layout(int fn, int dtype, int64_t D, Layout& L, std::string& err) {
   L.off_rowf = (int)o; o += align16((size_t)R * 8);
   L.off_flag = (int)o; o += align16((size_t)R * 4);
   L.off_red = (int)o; o += 128;
+  L.off_bar = (int)o; o += 16;
   L.smem = o;
   return true;
 }
@@ -322,9 +333,15 @@ struct psso_ctx {
   bool bound;
   cudaStream_t stream;
   int device, num_sms;
-  Layout L;
-  const void* tile_fn;
+  Layout L;   // k_tile
+  Layout LF;  // fused kernel (k_fused when rows vectorize, else k_tile<fused>)
+  const void* tile_fn;   // runtime-mode tile kernel (init, phases, evaluation)
+  const void* fused_fn;  // fused iteration kernel (the hot path)
+  const void* init_fn;   // initialization kernel (k_chain<INIT> or k_tile)
+  bool chain;            // fused/init run the register-resident chain kernel
   int grid;
+  int fused_grid;
+  int init_grid;
   int argmin_grid;
   int nslots;
   double* slot_f;
@@ -382,10 +399,10 @@ int validate(const psso_config* c, std::string& err) {
   return PSSO_OK;
 }
 
-TileParams tile_params(psso_ctx* c, int mode, int64_t t, const int64_t* t_dev) {
+TileParams tile_params(psso_ctx* c, int mode, int64_t t, const int64_t* t_dev, bool fused = false) {
   TileParams p;
   std::memset(&p, 0, sizeof(p));
-  const Layout& L = c->L;
+  const Layout& L = fused ? c->LF : c->L;
   p.X = c->buf.sol;
   p.P = c->buf.pbests;
   p.sol_f = c->buf.sol_f;
@@ -417,13 +434,18 @@ TileParams tile_params(psso_ctx* c, int mode, int64_t t, const int64_t* t_dev) {
   p.off_xs = L.off_xs; p.off_scr = L.off_scr; p.off_gb = L.off_gb; p.off_hb = L.off_hb;
   p.off_hf = L.off_hf; p.off_leaf = L.off_leaf; p.off_rowf = L.off_rowf; p.off_flag = L.off_flag;
   p.off_red = L.off_red;
+  p.off_bar = L.off_bar;
+  p.stage_bytes = L.stage_bytes;
+  p.pre = L.pre ? 1 : 0;
+  p.div_n = make_div((uint32_t)L.plan.n);
   p.plan = L.plan;
   return p;
 }
 
-int launch_tile(psso_ctx* c, const TileParams& p) {
+int launch_tile(psso_ctx* c, const TileParams& p, bool fused = false) {
   void* args[] = {(void*)&p};
-  CK(c, cudaLaunchKernel(c->tile_fn, dim3(c->grid), dim3(NT), args, c->L.smem, c->stream));
+  CK(c, cudaLaunchKernel(fused ? c->fused_fn : c->tile_fn, dim3(fused ? c->fused_grid : c->grid),
+                         dim3(NT), args, fused ? c->LF.smem : c->L.smem, c->stream));
   c->launches++;
   return PSSO_OK;
 }
@@ -477,7 +499,7 @@ int launch_fused(psso_ctx* c, int64_t t, int64_t* t_dev) {
     }
     CK(c, cudaEventRecord(c->ev[c->ev_used], c->stream));
   }
-  int rc = launch_tile(c, tile_params(c, fused_mode(c), t, t_dev));
+  int rc = launch_tile(c, tile_params(c, fused_mode(c), t, t_dev, true), true);
   if (rc) return rc;
   if (timed) {
     CK(c, cudaEventRecord(c->ev[c->ev_used + 1], c->stream));
@@ -488,7 +510,7 @@ int launch_fused(psso_ctx* c, int64_t t, int64_t* t_dev) {
 
 int fused_step(psso_ctx* c, int64_t t, int64_t* t_dev) {
   if (int rc = launch_fused(c, t, t_dev)) return rc;
-  return launch_gbest(c, gb_params(c, t, t_dev, 0, c->grid));
+  return launch_gbest(c, gb_params(c, t, t_dev, 0, c->fused_grid));
 }
 
 }  // namespace
@@ -518,32 +540,76 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
   c->launches = 0;
   c->profiling = false;
   c->ev_used = 0;
-  if (!make_layout(cfg->fn_id, cfg->dtype, cfg->nvar, c->L, err)) {
+  if (!make_layout(cfg->fn_id, cfg->dtype, cfg->nvar, false, c->L, err)) {
     delete c;
     return fail(nullptr, PSSO_E_UNSUPPORTED, err);
   }
-  c->tile_fn = tile_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, c->L.V);
-  if (!c->tile_fn) {
+  {  // the TMA kernel needs 16-byte rows (vectorized V > 1); else the fused k_tile
+    const bool tma = c->L.V > 1;
+    if (!make_layout(cfg->fn_id, cfg->dtype, cfg->nvar, tma, c->LF, err)) {
+      delete c;
+      return fail(nullptr, PSSO_E_UNSUPPORTED, err);
+    }
+  }
+  c->tile_fn = tile_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, c->L.V, false);
+  c->fused_fn = tile_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, c->L.V, true);
+  c->init_fn = c->tile_fn;
+  c->chain = false;
+  {  // register-resident chain kernel: one pairwise leaf of position-local terms
+    const int64_t D = cfg->nvar;
+    const int M = D <= 32 ? 4 : D <= 64 ? 8 : D <= 128 ? 16 : 0;
+    const char* off = std::getenv("PSSO_NO_CHAIN");
+    if (M && terms_of(cfg->fn_id, D) <= 128 && !(off && *off && *off != '0')) {
+      const void* f = chain_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, M, false);
+      const void* i = chain_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, M, true);
+      if (f && i) {
+        c->fused_fn = f;
+        c->init_fn = i;
+        c->chain = true;
+        const int es = cfg->dtype == PSSO_F64 ? 8 : 4;
+        c->LF.off_red = (int)align16((size_t)D * es);
+        c->LF.smem = (size_t)c->LF.off_red + 128;
+      }
+    }
+  }
+  if (!c->tile_fn || !c->fused_fn) {
     delete c;
     return fail(nullptr, PSSO_E_UNSUPPORTED, "no kernel instantiation for this configuration");
   }
   cudaError_t e;
   if ((e = cudaGetDevice(&c->device)) != cudaSuccess ||
       (e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device)) != cudaSuccess ||
-      (e = cudaFuncSetAttribute(c->tile_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->L.smem)) != cudaSuccess) {
+      (e = cudaFuncSetAttribute(c->tile_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->L.smem)) != cudaSuccess ||
+      (e = cudaFuncSetAttribute(c->fused_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->LF.smem)) != cudaSuccess) {
     delete c;
     return cuda_fail(nullptr, e, "psso_create");
   }
-  int per_sm = 0;
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, c->tile_fn, NT, c->L.smem)) != cudaSuccess || per_sm < 1) {
+  int per_sm = 0, per_sm_fused = 0;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, c->tile_fn, NT, c->L.smem)) != cudaSuccess ||
+      (e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_fused, c->fused_fn, NT, c->LF.smem)) != cudaSuccess ||
+      per_sm < 1 || per_sm_fused < 1) {
     delete c;
     return e != cudaSuccess ? cuda_fail(nullptr, e, "occupancy") : fail(nullptr, PSSO_E_UNSUPPORTED, "tile kernel cannot be resident");
   }
   const int64_t rows = cfg->row_hi - cfg->row_lo;
   const int64_t ntiles = (rows + c->L.R - 1) / c->L.R;
   c->grid = (int)std::min<int64_t>(ntiles, (int64_t)per_sm * c->num_sms);
+  const int64_t ntiles_f = (rows + c->LF.R - 1) / c->LF.R;
+  c->fused_grid = (int)std::min<int64_t>(ntiles_f, (int64_t)per_sm_fused * c->num_sms);
+  c->init_grid = c->grid;
+  if (c->chain) {  // 4 particles per warp, 8 warps per CTA
+    int per_sm_init = 0;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_init, c->init_fn, NT, c->LF.smem)) != cudaSuccess ||
+        per_sm_init < 1) {
+      delete c;
+      return e != cudaSuccess ? cuda_fail(nullptr, e, "occupancy") : fail(nullptr, PSSO_E_UNSUPPORTED, "chain kernel cannot be resident");
+    }
+    const int64_t nctas = (rows + 4 * (NT / 32) - 1) / (4 * (NT / 32));
+    c->fused_grid = (int)std::min<int64_t>(nctas, (int64_t)per_sm_fused * c->num_sms);
+    c->init_grid = (int)std::min<int64_t>(nctas, (int64_t)per_sm_init * c->num_sms);
+  }
   c->argmin_grid = (int)std::min<int64_t>((rows + 255) / 256, 4 * c->num_sms);
-  c->nslots = std::max(c->grid, c->argmin_grid);
+  c->nslots = std::max(std::max(std::max(c->grid, c->fused_grid), c->init_grid), c->argmin_grid);
   c->Kw = k53(cfg->cw); c->Kp = k53(cfg->cp); c->Kg = k53(cfg->cg);
   c->Kw32 = k32(cfg->cw); c->Kp32 = k32(cfg->cp); c->Kg32 = k32(cfg->cg);
   c->aux = nullptr;
@@ -596,13 +662,23 @@ int psso_bind(psso_ctx* c, const psso_buffers* b, void* stream) {
   return PSSO_OK;
 }
 
+// initialization kernel: positions from the INIT stream, fitness, candidates
+static int launch_init(psso_ctx* c) {
+  if (!c->chain) return launch_tile(c, tile_params(c, M_INIT | M_EVAL | M_CAND | M_SOLF, -1, nullptr));
+  TileParams p = tile_params(c, M_INIT | M_EVAL | M_CAND | M_SOLF, -1, nullptr, true);
+  void* args[] = {(void*)&p};
+  CK(c, cudaLaunchKernel(c->init_fn, dim3(c->init_grid), dim3(NT), args, c->LF.smem, c->stream));
+  c->launches++;
+  return PSSO_OK;
+}
+
 int psso_init(psso_ctx* c) {
   if (int rc = need_bound(c)) return rc;
   k_set_u64<<<1, 1, 0, c->stream>>>(c->bad, ~0ull);
   c->launches++;
-  int rc = launch_tile(c, tile_params(c, M_INIT | M_EVAL | M_CAND | M_SOLF, -1, nullptr));
+  int rc = launch_init(c);
   if (rc) return rc;
-  GbParams g = gb_params(c, -1, nullptr, 1, c->grid);
+  GbParams g = gb_params(c, -1, nullptr, 1, c->chain ? c->init_grid : c->grid);
   g.traj = nullptr;
   return launch_gbest(c, g);
 }
@@ -690,8 +766,8 @@ int64_t psso_candidate_bytes(const psso_config* cfg) {
   return 16 + ((cfg->nvar * es + 15) / 16) * 16;
 }
 
-static int local_cand(psso_ctx* c, void* cand) {
-  GbParams g = gb_params(c, -1, nullptr, 0, c->grid);
+static int local_cand(psso_ctx* c, void* cand, int nslots) {
+  GbParams g = gb_params(c, -1, nullptr, 0, nslots);
   unsigned char* rec = (unsigned char*)cand;
   if (c->cfg.dtype == PSSO_F64)
     k_local_cand<double><<<1, GB_THREADS, 0, c->stream>>>(g, rec);
@@ -707,16 +783,16 @@ int psso_init_local(psso_ctx* c, void* cand) {
   if (!cand) return fail(c, PSSO_E_INVALID, "null candidate buffer");
   k_set_u64<<<1, 1, 0, c->stream>>>(c->bad, ~0ull);
   c->launches++;
-  int rc = launch_tile(c, tile_params(c, M_INIT | M_EVAL | M_CAND | M_SOLF, -1, nullptr));
+  int rc = launch_init(c);
   if (rc) return rc;
-  return local_cand(c, cand);
+  return local_cand(c, cand, c->chain ? c->init_grid : c->grid);
 }
 
 int psso_step_local(psso_ctx* c, int64_t t, void* cand) {
   if (int rc = need_bound(c)) return rc;
   if (!cand) return fail(c, PSSO_E_INVALID, "null candidate buffer");
   if (int rc = launch_fused(c, t, nullptr)) return rc;
-  return local_cand(c, cand);
+  return local_cand(c, cand, c->fused_grid);
 }
 
 int psso_apply_candidates(psso_ctx* c, int64_t t, const void* cands, int32_t ncand, int32_t is_init) {

@@ -22,6 +22,12 @@
 namespace psso {
 
 constexpr int NT = 256;            // threads per CTA of k_tile
+#ifndef PSSO_U
+#define PSSO_U 4  // phase-A chunks loaded per thread before compute
+#endif
+#ifndef PSSO_MINB
+#define PSSO_MINB 4  // resident CTAs per SM the register budget is sized for
+#endif
 constexpr int MAX_LEAVES = 64;     // pairwise-sum leaves per row (D <= ~8192)
 constexpr int MAX_OPS = 2 * MAX_LEAVES;
 
@@ -80,6 +86,7 @@ struct TileParams {
   FastDiv div_cpr;
   FastDiv div_G;
   FastDiv div_D;
+  FastDiv div_n;               // by the row's term count (plan.n)
   int32_t fn_pad;
   uint64_t seed;
   uint64_t Kw, Kp, Kg;         // reference mode: branch k = h >> 11 compared < K
@@ -93,7 +100,10 @@ struct TileParams {
   unsigned long long* bad;     // first non-finite key ((t+1) << 40 | i)
   const double* aux;           // f7: 1/sqrt(1..D) table
   int32_t off_xs, off_scr, off_gb, off_hb, off_hf, off_leaf, off_rowf, off_flag, off_red;
-  int32_t pad2;
+  int32_t pre;                 // heavy terms precomputed by all threads (see tile_fitness)
+  int32_t off_bar;             // k_fused: two mbarriers; stages start at off_xs
+  int32_t stage_bytes;         // k_fused: bytes of one stage (X tile + P tile)
+  int32_t pad3;
   Plan plan;
 };
 
@@ -194,14 +204,62 @@ __device__ __forceinline__ void stg_stream(T* p, const VecT<T, V>& v) {
 // ----------------------------------------------------------- objectives ----
 // Terms follow benchmarks.py:109-166 in numpy's elementwise order.
 
+// ---------------------------------------------------------- sin / cos ----
+// fp64 sin/cos for the objectives' moderate arguments: Cody-Waite reduction by
+// pi/2 with FMA (|y| <= 1e6) and the fdlibm __kernel_sin/__kernel_cos minimax
+// polynomials (|r| <= pi/4, < 1 ulp).  ~25 fp64 instructions instead of the
+// ~75 the general libdevice routine issues on this path; larger arguments
+// fall back to libdevice.  Agreement with glibc/numpy is to ulps either way
+// (the parity tolerance of the transcendental objectives).
+__device__ __forceinline__ void sincos_reduced(double y, double& s, double& c, int& q) {
+  const double t = __fma_rn(y, 6.36619772367581382433e-01, 6755399441055744.0);  // 1.5 * 2^52
+  const double kd = __dsub_rn(t, 6755399441055744.0);
+  q = __double2loint(t);
+  double r = __fma_rn(-kd, 1.5707963267948966, y);
+  r = __fma_rn(-kd, 6.123233995736766e-17, r);
+  const double z = __dmul_rn(r, r);
+  // sin(r) = r + r^3 (S1 + z (S2 + ... + z S6))
+  double ps = __fma_rn(z, 1.58969099521155010221e-10, -2.50507602534068634195e-08);
+  ps = __fma_rn(z, ps, 2.75573137070700676789e-06);
+  ps = __fma_rn(z, ps, -1.98412698298579493134e-04);
+  ps = __fma_rn(z, ps, 8.33333333332248946124e-03);
+  ps = __fma_rn(z, ps, -1.66666666666666324348e-01);
+  s = __fma_rn(__dmul_rn(z, r), ps, r);
+  // cos(r) = w + (((1 - w) - hz) + z^2 (C1 + z (C2 + ... + z C6))), w = 1 - z/2
+  double pc = __fma_rn(z, -1.13596475577881948265e-11, 2.08757232129817482790e-09);
+  pc = __fma_rn(z, pc, -2.75573143513906633035e-07);
+  pc = __fma_rn(z, pc, 2.48015872894767294178e-05);
+  pc = __fma_rn(z, pc, -1.38888888888741095749e-03);
+  pc = __fma_rn(z, pc, 4.16666666666666019037e-02);
+  const double hz = __dmul_rn(0.5, z);
+  const double w = __dsub_rn(1.0, hz);
+  c = __dadd_rn(w, __fma_rn(__dmul_rn(z, z), pc, __dsub_rn(__dsub_rn(1.0, w), hz)));
+}
+__device__ __forceinline__ double fast_cos(double y) {
+  if (!(fabs(y) <= 1.0e6)) return cos(y);
+  double s, c;
+  int q;
+  sincos_reduced(y, s, c, q);
+  const double v = (q & 1) ? s : c;
+  return ((q + 1) & 2) ? -v : v;
+}
+__device__ __forceinline__ double fast_sin(double y) {
+  if (!(fabs(y) <= 1.0e6)) return sin(y);
+  double s, c;
+  int q;
+  sincos_reduced(y, s, c, q);
+  const double v = (q & 1) ? c : s;
+  return (q & 2) ? -v : v;
+}
+
 template <typename T> struct Num;
 template <> struct Num<double> {
   static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
   static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
   static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
   static __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
-  static __device__ __forceinline__ double cos_(double a) { return cos(a); }
-  static __device__ __forceinline__ double sin_(double a) { return sin(a); }
+  static __device__ __forceinline__ double cos_(double a) { return fast_cos(a); }
+  static __device__ __forceinline__ double sin_(double a) { return fast_sin(a); }
   static __device__ __forceinline__ double exp_(double a) { return exp(a); }
   static __device__ __forceinline__ double sqrt_(double a) { return __dsqrt_rn(a); }
   static __device__ __forceinline__ double pow4(double a) { return pow(a, 4.0); }
@@ -220,45 +278,63 @@ template <> struct Num<float> {
   static constexpr float TWO_PI = 6.2831855f;
 };
 
-// term #e of the row's first (and, for f6, second) pairwise sum.
+// Objective terms, in numpy's elementwise order (benchmarks.py:109-166).
+// "Heavy" terms (transcendentals) may be precomputed by all threads into a
+// term buffer before the chain pass when the chains alone would leave threads
+// idle; cheap terms are always formed inside the chains.
+template <int FN>
+__host__ __device__ constexpr bool heavy_terms() { return FN == 5 || FN == 6 || FN == 8 || FN == 9; }
+__host__ __device__ constexpr bool two_sums(int FN) { return FN == 6; }
+
 template <typename T, int FN>
-__device__ __forceinline__ T term1(const T* x, int e) {
+__device__ __forceinline__ T heavy_term(const T* x, int e) {
+  using N = Num<T>;
+  if constexpr (FN == 5) {
+    const T v = x[e];
+    return N::sub(N::mul(v, v), N::mul((T)10, N::cos_(N::mul((T)N::TWO_PI, v))));
+  } else if constexpr (FN == 6) {
+    return N::cos_(N::mul((T)N::TWO_PI, x[e]));
+  } else if constexpr (FN == 8) {
+    const T a = x[4 * e], b = x[4 * e + 1], c = x[4 * e + 2], d = x[4 * e + 3];
+    const T t1 = N::add(a, N::mul((T)10, b));
+    const T t2 = N::sub(c, d);
+    const T t3 = N::sub(b, N::mul((T)2, c));
+    const T t4 = N::sub(a, d);
+    return N::add(N::add(N::add(N::mul(t1, t1), N::mul((T)5, N::mul(t2, t2))), N::pow4(t3)),
+                  N::mul((T)10, N::pow4(t4)));
+  } else if constexpr (FN == 9) {
+    const T v = x[e];
+    return N::mul(v, N::sin_(N::sqrt_(fabs(v))));
+  } else {
+    return (T)0;
+  }
+}
+
+// term #e of the row's first pairwise sum; `buf` holds precomputed terms
+// (f3 always, heavy objectives when `pre`).
+template <typename T, int FN>
+__device__ __forceinline__ T term1(const T* x, const T* buf, int e, bool pre) {
   using N = Num<T>;
   if constexpr (FN == 1 || FN == 0 || FN == 6 || FN == 7) {
     return N::mul(x[e], x[e]);
   } else if constexpr (FN == 2) {
     return N::mul(N::mul((T)(e + 1), x[e]), x[e]);
   } else if constexpr (FN == 3) {
-    return x[e];  // f3 sums precomputed c*c terms (scratch passed as x)
+    return buf[e];
   } else if constexpr (FN == 4) {
-    T h = x[e];
-    T d = N::sub(x[e + 1], N::mul(h, h));
-    T o = N::sub((T)1, h);
+    const T h = x[e];
+    const T d = N::sub(x[e + 1], N::mul(h, h));
+    const T o = N::sub((T)1, h);
     return N::add(N::mul(N::mul((T)100, d), d), N::mul(o, o));
-  } else if constexpr (FN == 5) {
-    T v = x[e];
-    return N::sub(N::mul(v, v), N::mul((T)10, N::cos_(N::mul((T)N::TWO_PI, v))));
-  } else if constexpr (FN == 8) {
-    T a = x[4 * e], b = x[4 * e + 1], c = x[4 * e + 2], d = x[4 * e + 3];
-    T t1 = N::add(a, N::mul((T)10, b));
-    T t2 = N::sub(c, d);
-    T t3 = N::sub(b, N::mul((T)2, c));
-    T t4 = N::sub(a, d);
-    return N::add(N::add(N::add(N::mul(t1, t1), N::mul((T)5, N::mul(t2, t2))), N::pow4(t3)),
-                  N::mul((T)10, N::pow4(t4)));
-  } else {  // FN == 9
-    T v = x[e];
-    return N::mul(v, N::sin_(N::sqrt_(fabs(v))));
+  } else {  // 5, 8, 9
+    return pre ? buf[e] : heavy_term<T, FN>(x, e);
   }
 }
 
 template <typename T, int FN>
-__device__ __forceinline__ T term2(const T* x, int e) {  // f6 only
-  using N = Num<T>;
-  return N::cos_(N::mul((T)N::TWO_PI, x[e]));
+__device__ __forceinline__ T term2(const T* x, const T* buf, int e, bool pre) {  // f6 only
+  return pre ? buf[e] : heavy_term<T, 6>(x, e);
 }
-
-__host__ __device__ constexpr bool two_sums(int FN) { return FN == 6; }
 
 // Final per-row fitness from the pairwise sums (s2 only for f6; prod for f7).
 template <typename T, int FN>
@@ -267,9 +343,9 @@ __device__ __forceinline__ double finish(T s1, T s2, T prod, int D, const T* x, 
   if constexpr (FN == 5) {
     return (double)N::add(N::mul((T)10, (T)D), s1);
   } else if constexpr (FN == 6) {
-    T rms = N::sqrt_(N::div(s1, (T)D));
-    T mc = N::div(s2, (T)D);
-    T a = N::mul((T)-20, N::exp_(N::mul((T)-0.2, rms)));
+    const T rms = N::sqrt_(N::div(s1, (T)D));
+    const T mc = N::div(s2, (T)D);
+    const T a = N::mul((T)-20, N::exp_(N::mul((T)-0.2, rms)));
     return (double)N::add(N::add(N::sub(a, N::exp_(mc)), (T)20), (T)2.718281828459045);
   } else if constexpr (FN == 7) {
     return (double)N::add(N::sub(N::div(s1, (T)4000), prod), (T)1);
@@ -287,37 +363,48 @@ __device__ __forceinline__ bool lex_less(double fa, int64_t ia, double fb, int64
 }
 
 // ------------------------------------------------------------ phase B ----
-// Fitness of the Rt rows held in smem (row r at xs + r*S), numpy order:
-// each leaf of >= 8 terms is reduced by 8 consecutive lanes (lane k owns the
-// strided accumulator r[k] = t[k] + t[k+8] + ..., summed in order), the 8
-// accumulators combine as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) through xor
-// shuffles (commutative, so bit-identical), the leader lane adds the leaf's
-// tail sequentially, and the row leader combines leaves in recursion order.
-template <typename T, int FN>
-__device__ void tile_fitness(const TileParams& p, const T* xs, double* scr, double* leafv,
-                             double* rowf, int Rt) {
+// Fitness of the Rt rows held in smem (row r at x + r*SX; term buffer rows at
+// buf + r*S), numpy order: each leaf of >= 8 terms is reduced by 8
+// consecutive lanes (lane k owns the strided accumulator r[k] = t[k] + t[k+8]
+// + ..., summed in order), the 8 accumulators combine as
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) through xor shuffles (commutative, so
+// bit-identical), the leader lane adds the leaf's tail sequentially, and the
+// row leader combines leaves in recursion order.  `pre`: heavy terms are
+// first computed by all NTH threads into `buf`.
+template <typename T, int FN, int NTH>
+__device__ void tile_fitness(const TileParams& p, const T* xsrc, int SX, T* buf, double* leafv,
+                             double* rowf, int Rt, bool pre) {
   using N = Num<T>;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const Plan& pl = p.plan;
   const int NL = pl.nleaves, S = p.S, D = p.D;
-  T* tscr = reinterpret_cast<T*>(scr);
 
   if constexpr (FN == 3) {  // c = cumsum(x) sequentially (numpy), terms c*c
-    for (int r = tid; r < Rt; r += NT) {
-      const T* x = xs + r * S;
+    for (int r = tid; r < Rt; r += NTH) {
+      const T* x = xsrc + r * SX;
       T c = x[0];
-      tscr[r * S] = N::mul(c, c);
+      buf[r * S] = N::mul(c, c);
       for (int j = 1; j < D; ++j) {
         c = N::add(c, x[j]);
-        tscr[r * S + j] = N::mul(c, c);
+        buf[r * S + j] = N::mul(c, c);
       }
     }
     __syncthreads();
   }
-  const T* src = (FN == 3) ? tscr : xs;
+  if constexpr (heavy_terms<FN>()) {
+    if (pre) {  // all threads: heavy terms -> buf (row-major, padded stride)
+      const int n = Rt * pl.n;
+      for (int e = tid; e < n; e += NTH) {
+        const int r = (int)p.div_n.div((uint32_t)e);
+        const int j = e - r * pl.n;
+        buf[r * S + j] = heavy_term<T, FN>(xsrc + r * SX, j);
+      }
+      __syncthreads();
+    }
+  }
 
   const int total = Rt * p.G;
-  for (int base = warp * 32; base < total; base += NT) {
+  for (int base = warp * 32; base < total; base += NTH) {
     const int c = base + lane;
     const bool active = c < total;
     int row = 0, leaf = 0, k = 0, off = 0, len = 0;
@@ -329,14 +416,15 @@ __device__ void tile_fitness(const TileParams& p, const T* xs, double* scr, doub
       k = q & 7;
       off = pl.leaf_off[leaf];
       len = pl.leaf_len[leaf];
-      const T* x = src + row * S;
+      const T* x = xsrc + row * SX;
+      const T* bb = buf + row * S;
       const int mlen = len >> 3;  // chain length (leaves >= 8)
       if (mlen > 0) {
-        a1 = term1<T, FN>(x, off + k);
-        if constexpr (two_sums(FN)) a2 = term2<T, FN>(x, off + k);
+        a1 = term1<T, FN>(x, bb, off + k, pre);
+        if constexpr (two_sums(FN)) a2 = term2<T, FN>(x, bb, off + k, pre);
         for (int m = 1; m < mlen; ++m) {
-          a1 = N::add(a1, term1<T, FN>(x, off + k + 8 * m));
-          if constexpr (two_sums(FN)) a2 = N::add(a2, term2<T, FN>(x, off + k + 8 * m));
+          a1 = N::add(a1, term1<T, FN>(x, bb, off + k + 8 * m, pre));
+          if constexpr (two_sums(FN)) a2 = N::add(a2, term2<T, FN>(x, bb, off + k + 8 * m, pre));
         }
       }
     }
@@ -349,13 +437,14 @@ __device__ void tile_fitness(const TileParams& p, const T* xs, double* scr, doub
       a2 = N::add(a2, __shfl_xor_sync(0xffffffffu, a2, 4));
     }
     if (active && k == 0) {
-      const T* x = src + row * S;
+      const T* x = xsrc + row * SX;
+      const T* bb = buf + row * S;
       T r1 = (len >= 8) ? a1 : (T)0;
       T r2 = (len >= 8) ? a2 : (T)0;
       const int tail0 = off + (len & ~7) * (len >= 8 ? 1 : 0);
       for (int e = tail0; e < off + len; ++e) {
-        r1 = N::add(r1, term1<T, FN>(x, e));
-        if constexpr (two_sums(FN)) r2 = N::add(r2, term2<T, FN>(x, e));
+        r1 = N::add(r1, term1<T, FN>(x, bb, e, pre));
+        if constexpr (two_sums(FN)) r2 = N::add(r2, term2<T, FN>(x, bb, e, pre));
       }
       leafv[(row * NL + leaf) * 2] = (double)r1;
       leafv[(row * NL + leaf) * 2 + 1] = (double)r2;
@@ -364,15 +453,15 @@ __device__ void tile_fitness(const TileParams& p, const T* xs, double* scr, doub
 
   if constexpr (FN == 7) {  // factors cos(x * inv) for the sequential product
     const int n = Rt * D;
-    for (int e = tid; e < n; e += NT) {
+    for (int e = tid; e < n; e += NTH) {
       const int r = (int)p.div_D.div((uint32_t)e);
       const int j = e - r * D;
-      tscr[r * S + j] = N::cos_(N::mul(xs[r * S + j], (T)p.aux[j]));
+      buf[r * S + j] = N::cos_(N::mul(xsrc[r * SX + j], (T)p.aux[j]));
     }
   }
   __syncthreads();
 
-  for (int r = tid; r < Rt; r += NT) {
+  for (int r = tid; r < Rt; r += NTH) {
     T s1, s2 = (T)0, prod = (T)1;
     const double* lv = leafv + r * NL * 2;
     if (NL == 1) {
@@ -397,17 +486,88 @@ __device__ void tile_fitness(const TileParams& p, const T* xs, double* scr, doub
       s2 = st2[0];
     }
     if constexpr (FN == 7) {
-      const T* f = tscr + r * S;
+      const T* f = buf + r * S;
       for (int j = 0; j < D; ++j) prod = N::mul(prod, f[j]);
     }
-    rowf[r] = finish<T, FN>(s1, s2, prod, D, xs + r * S, p.probe_level);
+    rowf[r] = finish<T, FN>(s1, s2, prod, D, xsrc + r * SX, p.probe_level);
   }
 }
 
-// -------------------------------------------------------------- k_tile ----
+// ------------------------------------------------------- phase A chunk ----
+// One V-wide chunk of one row: the keyed branch draw and four-way select of
+// core.py:138-173, branch-free.  Both the branch hash and the fresh hash are
+// evaluated for every coordinate (a warp executes the fresh path whenever any
+// lane needs it, so predication is free), and the cumulative thresholds turn
+// the select chain into three monotone compares:
+//   k >= Kw -> pbest, k >= Kp -> gbest, k >= Kg -> fresh   (else keep x)
+template <typename T, int V, int RNG>
+__device__ __forceinline__ VecT<T, V> search_chunk(const TileParams& p, const VecT<T, V>& x,
+                                                   const VecT<T, V>& pb, const VecT<T, V>& gv,
+                                                   uint64_t hr, uint64_t fr, int col, uint64_t gi,
+                                                   int64_t t) {
+  VecT<T, V> nv;
+  if constexpr (RNG == 0) {
+    uint64_t g = GAMMA * (uint64_t)(col + 1);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const uint64_t kb = mix64(hr ^ g) >> 11;
+      const double fresh = __dadd_rn(p.var_min, __dmul_rn(p.span, unit53(mix64(fr ^ g))));
+      T a = x.v[v];
+      a = kb >= p.Kw ? pb.v[v] : a;
+      a = kb >= p.Kp ? gv.v[v] : a;
+      a = kb >= p.Kg ? (T)fresh : a;
+      nv.v[v] = a;
+      g += GAMMA;
+    }
+  } else {
+    Philox4 w;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int j = col + v;
+      if (v == 0 || (j & 1) == 0)
+        w = philox4x32_10((uint32_t)(j >> 1), (uint32_t)gi, (uint32_t)(gi >> 32), (uint32_t)t,
+                          (uint32_t)p.seed, (uint32_t)(p.seed >> 32));
+      const uint64_t kb = w.w[j & 1];
+      const double raw = __dmul_rn((double)w.w[2 + (j & 1)], 2.3283064365386963e-10);
+      const double fresh = __dadd_rn(p.var_min, __dmul_rn(p.span, raw));
+      T a = x.v[v];
+      a = kb >= p.Kw32 ? pb.v[v] : a;
+      a = kb >= p.Kp32 ? gv.v[v] : a;
+      a = kb >= p.Kg32 ? (T)fresh : a;
+      nv.v[v] = a;
+    }
+  }
+  return nv;
+}
 
-template <typename T, int FN, int RNG, int V>
-__global__ void __launch_bounds__(NT) k_tile(const __grid_constant__ TileParams p) {
+// Initial positions var_min + span * u(INIT, 0, i, j) (core.py:198-199).
+template <typename T, int V, int RNG>
+__device__ __forceinline__ VecT<T, V> init_chunk(const TileParams& p, uint64_t hr, int col,
+                                                 uint64_t gi) {
+  VecT<T, V> nv;
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    uint64_t h;
+    if constexpr (RNG == 0) {
+      h = mix64(hr ^ (GAMMA * (uint64_t)(col + v + 1)));
+    } else {
+      const int j = col + v;
+      Philox4 w = philox4x32_10((uint32_t)(j >> 1), (uint32_t)gi, (uint32_t)(gi >> 32),
+                                0xFFFFFFFFu, (uint32_t)p.seed, (uint32_t)(p.seed >> 32));
+      const int s = (j & 1) * 2;
+      h = ((uint64_t)w.w[s] << 32) | w.w[s + 1];
+    }
+    nv.v[v] = (T)__dadd_rn(p.var_min, __dmul_rn(p.span, unit53(h)));
+  }
+  return nv;
+}
+
+// -------------------------------------------------------------- k_tile ----
+// FUSED = the hot path (SEARCH|EVAL|PBEST|CAND known at compile time);
+// otherwise the mode mask comes from the launch (init, phase API, evaluation).
+
+template <typename T, int FN, int RNG, int V, bool FUSED>
+__global__ void __launch_bounds__(NT, PSSO_MINB) k_tile(const __grid_constant__ TileParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   T* xs = reinterpret_cast<T*>(smem + p.off_xs);
   double* scr = reinterpret_cast<double*>(smem + p.off_scr);
@@ -418,8 +578,9 @@ __global__ void __launch_bounds__(NT) k_tile(const __grid_constant__ TileParams 
   double* rowf = reinterpret_cast<double*>(smem + p.off_rowf);
   int* flag = reinterpret_cast<int*>(smem + p.off_flag);
 
-  const int tid = threadIdx.x;
-  const int mode = p.mode;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = NT / 32;
+  const int mode = FUSED ? (M_SEARCH | M_EVAL | M_PBEST | M_CAND | (p.mode & M_SOLF)) : p.mode;
   const int D = p.D, S = p.S, cpr = p.cpr;
   // a non-finite fitness already stopped the run (core.py:190-193 raises at
   // the first one): later iterations leave the state as it was
@@ -466,88 +627,37 @@ __global__ void __launch_bounds__(NT) k_tile(const __grid_constant__ TileParams 
     T* Xt = X + r0 * (int64_t)D;
     T* Pt = P + r0 * (int64_t)D;
     const int nch = Rt * cpr;
-    constexpr int U = 4;
+    constexpr int U = PSSO_U;  // chunks in flight per thread
     for (int c0 = tid; c0 < nch; c0 += U * NT) {
       VecT<T, V> xv[U], pv[U];
+      int rows[U], cols[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int c = c0 + u * NT;
+        const int row = (int)p.div_cpr.div((uint32_t)c);
+        rows[u] = row;
+        cols[u] = (c - row * cpr) * V;
         if (c < nch && (mode & (M_SEARCH | M_LOAD))) {
-          const int row = (int)p.div_cpr.div((uint32_t)c);
-          const int col = (c - row * cpr) * V;
-          xv[u] = ldg_stream<T, V>(Xt + row * D + col);
-          if (mode & M_SEARCH) pv[u] = ldg_stream<T, V>(Pt + row * D + col);
+          xv[u] = ldg_stream<T, V>(Xt + row * D + cols[u]);
+          if (mode & M_SEARCH) pv[u] = ldg_stream<T, V>(Pt + row * D + cols[u]);
         }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int c = c0 + u * NT;
-        if (c >= nch) break;
-        const int row = (int)p.div_cpr.div((uint32_t)c);
-        const int col = (c - row * cpr) * V;
+        if (c0 + u * NT >= nch) break;
+        const int row = rows[u], col = cols[u];
         VecT<T, V> nv;
         if (mode & M_INIT) {
-          if constexpr (RNG == 0) {
-            const uint64_t hr = hbs[row];
-#pragma unroll
-            for (int v = 0; v < V; ++v) {
-              const uint64_t h = mix64(hr ^ (GAMMA * (uint64_t)(col + v + 1)));
-              nv.v[v] = (T)__dadd_rn(p.var_min, __dmul_rn(p.span, unit53(h)));
-            }
-          } else {
-            const uint64_t gi = (uint64_t)(gi0 + row);
-#pragma unroll
-            for (int v = 0; v < V; ++v) {
-              const int j = col + v;
-              Philox4 w = philox4x32_10((uint32_t)(j >> 1), (uint32_t)gi, (uint32_t)(gi >> 32),
-                                        0xFFFFFFFFu, (uint32_t)p.seed, (uint32_t)(p.seed >> 32));
-              const int s = (j & 1) * 2;
-              const uint64_t h = ((uint64_t)w.w[s] << 32) | w.w[s + 1];
-              nv.v[v] = (T)__dadd_rn(p.var_min, __dmul_rn(p.span, unit53(h)));
-            }
-          }
-          *reinterpret_cast<VecT<T, V>*>(Pt + row * D + col) = nv;
+          nv = init_chunk<T, V, RNG>(p, RNG == 0 ? hbs[row] : 0, col, (uint64_t)(gi0 + row));
+          stg_stream<T, V>(Pt + row * D + col, nv);
         } else if (mode & M_SEARCH) {
           const VecT<T, V> gv = *reinterpret_cast<const VecT<T, V>*>(gb + col);
-          if constexpr (RNG == 0) {
-            const uint64_t hr = hbs[row], fr = hfs[row];
-#pragma unroll
-            for (int v = 0; v < V; ++v) {
-              const uint64_t g = GAMMA * (uint64_t)(col + v + 1);
-              const uint64_t kb = mix64(hr ^ g) >> 11;
-              T val;
-              if (kb < p.Kw) val = xv[u].v[v];
-              else if (kb < p.Kp) val = pv[u].v[v];
-              else if (kb < p.Kg) val = gv.v[v];
-              else val = (T)__dadd_rn(p.var_min, __dmul_rn(p.span, unit53(mix64(fr ^ g))));
-              nv.v[v] = val;
-            }
-          } else {
-            const uint64_t gi = (uint64_t)(gi0 + row);
-            Philox4 w;
-#pragma unroll
-            for (int v = 0; v < V; ++v) {
-              const int j = col + v;
-              if (v == 0 || (j & 1) == 0)
-                w = philox4x32_10((uint32_t)(j >> 1), (uint32_t)gi, (uint32_t)(gi >> 32),
-                                  (uint32_t)t, (uint32_t)p.seed, (uint32_t)(p.seed >> 32));
-              const uint64_t kb = w.w[j & 1];
-              T val;
-              if (kb < p.Kw32) val = xv[u].v[v];
-              else if (kb < p.Kp32) val = pv[u].v[v];
-              else if (kb < p.Kg32) val = gv.v[v];
-              else {
-                const double raw = __dmul_rn((double)w.w[2 + (j & 1)], 2.3283064365386963e-10);
-                val = (T)__dadd_rn(p.var_min, __dmul_rn(p.span, raw));
-              }
-              nv.v[v] = val;
-            }
-          }
+          nv = search_chunk<T, V, RNG>(p, xv[u], pv[u], gv, RNG == 0 ? hbs[row] : 0,
+                                       RNG == 0 ? hfs[row] : 0, col, (uint64_t)(gi0 + row), t);
         } else {
           nv = xv[u];  // M_LOAD: evaluate existing positions
         }
-        if (mode & (M_INIT | M_SEARCH))
-          stg_stream<T, V>(Xt + row * D + col, nv);
+        if (mode & (M_INIT | M_SEARCH)) stg_stream<T, V>(Xt + row * D + col, nv);
         if (mode & M_EVAL) *reinterpret_cast<VecT<T, V>*>(xs + row * S + col) = nv;
       }
     }
@@ -555,7 +665,7 @@ __global__ void __launch_bounds__(NT) k_tile(const __grid_constant__ TileParams 
     __syncthreads();
 
     // ---- phase B: fitness in numpy order
-    tile_fitness<T, FN>(p, xs, scr, leafv, rowf, Rt);
+    tile_fitness<T, FN, NT>(p, xs, S, reinterpret_cast<T*>(scr), leafv, rowf, Rt, p.pre != 0);
     __syncthreads();
 
     // ---- phase C: bookkeeping per row, pbest rows from smem
@@ -579,20 +689,19 @@ __global__ void __launch_bounds__(NT) k_tile(const __grid_constant__ TileParams 
       flag[r] = imp;
       if ((mode & M_CAND) && lex_less(pf, gi, best_f, best_i)) { best_f = pf; best_i = gi; }
     }
-    if (mode & M_PBEST) {
+    if (mode & M_PBEST) {  // improved rows only, warp per row, straight from smem
       __syncthreads();
-      for (int c = tid; c < nch; c += NT) {
-        const int row = (int)p.div_cpr.div((uint32_t)c);
-        if (!flag[row]) continue;
-        const int col = (c - row * cpr) * V;
-        stg_stream<T, V>(Pt + row * D + col, *reinterpret_cast<const VecT<T, V>*>(xs + row * S + col));
+      for (int r = warp; r < Rt; r += NW) {
+        if (!flag[r]) continue;
+        for (int ch = lane; ch < cpr; ch += 32)
+          stg_stream<T, V>(Pt + r * D + ch * V, *reinterpret_cast<const VecT<T, V>*>(xs + r * S + ch * V));
       }
     }
   }
 
   if (mode & M_CAND) {  // deterministic CTA argmin -> one slot, no atomics
     double* red_f = reinterpret_cast<double*>(smem + p.off_red);
-    int64_t* red_i = reinterpret_cast<int64_t*>(smem + p.off_red + 8 * (NT / 32));
+    int64_t* red_i = reinterpret_cast<int64_t*>(smem + p.off_red + 8 * NW);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const double of = __shfl_xor_sync(0xffffffffu, best_f, o);
@@ -600,14 +709,453 @@ __global__ void __launch_bounds__(NT) k_tile(const __grid_constant__ TileParams 
       if (lex_less(of, oi, best_f, best_i)) { best_f = of; best_i = oi; }
     }
     __syncthreads();
-    if ((tid & 31) == 0) { red_f[tid >> 5] = best_f; red_i[tid >> 5] = best_i; }
+    if (lane == 0) { red_f[warp] = best_f; red_i[warp] = best_i; }
     __syncthreads();
     if (tid == 0) {
-      for (int w = 1; w < NT / 32; ++w)
+      for (int w = 1; w < NW; ++w)
         if (lex_less(red_f[w], red_i[w], best_f, best_i)) { best_f = red_f[w]; best_i = red_i[w]; }
       p.slot_f[blockIdx.x] = best_f;
       p.slot_i[blockIdx.x] = best_i;
     }
+  }
+}
+
+// ------------------------------------------------ TMA bulk-copy helpers ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine), completion counted on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// --------------------------------------------------------------- k_fused ----
+// The hot path: one fused PSSO iteration (SEARCH|EVAL|PBEST|CAND) as a
+// persistent kernel whose X and P tiles stream through a two-stage ring in
+// shared memory filled by TMA bulk copies (cp.async.bulk + mbarrier).  While
+// the CTA computes tile k, tile k+1 is already in flight, so HBM reads are
+// decoupled from the register file and the compute phases.  New positions are
+// written in place into the X stage (the smem copy phases B/C read) and
+// streamed to global X from registers; improved rows go to P from smem.
+template <typename T, int FN, int RNG, int V>
+__global__ void __launch_bounds__(NT, 2) k_fused(const __grid_constant__ TileParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  T* buf = reinterpret_cast<T*>(smem + p.off_scr);
+  T* gb = reinterpret_cast<T*>(smem + p.off_gb);
+  uint64_t* hbs = reinterpret_cast<uint64_t*>(smem + p.off_hb);
+  uint64_t* hfs = reinterpret_cast<uint64_t*>(smem + p.off_hf);
+  double* leafv = reinterpret_cast<double*>(smem + p.off_leaf);
+  double* rowf = reinterpret_cast<double*>(smem + p.off_rowf);
+  int* flag = reinterpret_cast<int*>(smem + p.off_flag);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + p.off_bar);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = NT / 32;
+  const int mode = M_SEARCH | M_EVAL | M_PBEST | M_CAND | (p.mode & M_SOLF);
+  const int D = p.D, cpr = p.cpr;
+  if (p.bad && *(volatile unsigned long long*)p.bad != ~0ull) return;  // run already failed
+  const int64_t t = p.t_dev ? *p.t_dev : p.t_arg;
+  T* __restrict__ X = reinterpret_cast<T*>(p.X);
+  T* __restrict__ P = reinterpret_cast<T*>(p.P);
+  const int64_t ntiles = (p.rows + p.R - 1) / p.R;
+  const uint32_t tile_elems = (uint32_t)p.R * (uint32_t)D;
+
+  auto stage_x = [&](int s) { return reinterpret_cast<T*>(smem + p.off_xs + s * p.stage_bytes); };
+  auto stage_p = [&](int s) {
+    return reinterpret_cast<T*>(smem + p.off_xs + s * p.stage_bytes) + tile_elems;
+  };
+  auto issue = [&](int64_t tile, int s) {  // one thread: X and P tiles -> stage s
+    if (tile >= ntiles) return;
+    const int64_t r0 = tile * p.R;
+    const uint32_t rt = (uint32_t)min((int64_t)p.R, p.rows - r0);
+    const uint32_t bytes = rt * (uint32_t)D * (uint32_t)sizeof(T);
+    mbar_expect_tx(&bar[s], 2 * bytes);
+    bulk_g2s(stage_x(s), X + r0 * D, bytes, &bar[s]);
+    bulk_g2s(stage_p(s), P + r0 * D, bytes, &bar[s]);
+  };
+
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
+    issue(blockIdx.x, 0);
+    issue(blockIdx.x + gridDim.x, 1);
+  }
+  uint64_t rootb = 0, rootf = 0;
+  if constexpr (RNG == 0) {
+    rootb = root64(p.seed, STREAM_BRANCH, (uint64_t)t);
+    rootf = root64(p.seed, STREAM_FRESH, (uint64_t)t);
+  }
+  {
+    const T* g = reinterpret_cast<const T*>(p.gbest);
+    for (int j = tid; j < D; j += NT) gb[j] = g[j];
+  }
+  __syncthreads();  // barriers initialized before anyone waits on them
+
+  double best_f = CUDART_INF;
+  int64_t best_i = INT64_MAX;
+  int k = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
+    const int s = k & 1;
+    const uint32_t parity = (k >> 1) & 1;
+    const int64_t r0 = tile * p.R;
+    const int Rt = (int)min((int64_t)p.R, p.rows - r0);
+    const int64_t gi0 = p.row_lo + r0;
+    T* Xs = stage_x(s);
+    const T* Ps = stage_p(s);
+
+    double pf_row = 0.0;  // this thread's row p_f, loaded early (used in phase C)
+    if (tid < Rt) pf_row = p.p_f[r0 + tid];
+    if constexpr (RNG == 0) {
+      for (int r = tid; r < Rt; r += NT) {
+        hbs[r] = fold64(rootb, (uint64_t)(gi0 + r));
+        hfs[r] = fold64(rootf, (uint64_t)(gi0 + r));
+      }
+    }
+    mbar_wait(&bar[s], parity);
+    __syncthreads();
+
+    // ---- phase A: select in place in the X stage, stream new X to HBM
+    T* Xt = X + r0 * (int64_t)D;
+    const int nch = Rt * cpr;
+    for (int c = tid; c < nch; c += NT) {
+      const int row = (int)p.div_cpr.div((uint32_t)c);
+      const int col = (c - row * cpr) * V;
+      const int e = row * D + col;
+      const VecT<T, V> xv = *reinterpret_cast<const VecT<T, V>*>(Xs + e);
+      const VecT<T, V> pv = *reinterpret_cast<const VecT<T, V>*>(Ps + e);
+      const VecT<T, V> gv = *reinterpret_cast<const VecT<T, V>*>(gb + col);
+      const VecT<T, V> nv = search_chunk<T, V, RNG>(p, xv, pv, gv, RNG == 0 ? hbs[row] : 0,
+                                                   RNG == 0 ? hfs[row] : 0, col,
+                                                   (uint64_t)(gi0 + row), t);
+      *reinterpret_cast<VecT<T, V>*>(Xs + e) = nv;
+      stg_stream<T, V>(Xt + e, nv);
+    }
+    __syncthreads();
+
+    // ---- phase B: fitness in numpy order (rows contiguous in the X stage)
+    tile_fitness<T, FN, NT>(p, Xs, D, buf, leafv, rowf, Rt, p.pre != 0);
+    __syncthreads();
+
+    // ---- phase C: pbest <= test, candidate, improved rows -> P
+    if (tid < Rt) {
+      const int r = tid;
+      const double f = rowf[r];
+      const int64_t gi = gi0 + r;
+      if (!isfinite(f) && p.bad)
+        atomicMin(p.bad, ((unsigned long long)(t + 1) << 40) | (unsigned long long)gi);
+      if (p.sol_f && ((mode & M_SOLF) || !isfinite(f))) p.sol_f[r0 + r] = f;
+      const int imp = (f <= pf_row);  // parallel.py:109, ties refresh
+      double pf = pf_row;
+      if (imp) { p.p_f[r0 + r] = f; pf = f; }
+      flag[r] = imp;
+      if (lex_less(pf, gi, best_f, best_i)) { best_f = pf; best_i = gi; }
+    }
+    __syncthreads();
+    T* Pt = P + r0 * (int64_t)D;
+    for (int r = warp; r < Rt; r += NW) {
+      if (!flag[r]) continue;
+      for (int ch = lane; ch < cpr; ch += 32)
+        stg_stream<T, V>(Pt + r * D + ch * V, *reinterpret_cast<const VecT<T, V>*>(Xs + r * D + ch * V));
+    }
+    __syncthreads();  // stage s fully consumed -> refill it with tile k+2
+    if (tid == 0) {
+      fence_proxy_async();
+      issue(tile + 2 * (int64_t)gridDim.x, s);
+    }
+  }
+
+  double* red_f = reinterpret_cast<double*>(smem + p.off_red);
+  int64_t* red_i = reinterpret_cast<int64_t*>(smem + p.off_red + 8 * NW);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double of = __shfl_xor_sync(0xffffffffu, best_f, o);
+    const int64_t oi = __shfl_xor_sync(0xffffffffu, best_i, o);
+    if (lex_less(of, oi, best_f, best_i)) { best_f = of; best_i = oi; }
+  }
+  if (lane == 0) { red_f[warp] = best_f; red_i[warp] = best_i; }
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < NW; ++w)
+      if (lex_less(red_f[w], red_i[w], best_f, best_i)) { best_f = red_f[w]; best_i = red_i[w]; }
+    p.slot_f[blockIdx.x] = best_f;
+    p.slot_i[blockIdx.x] = best_i;
+  }
+}
+
+// --------------------------------------------------------------- k_chain ----
+// Hot path for rows whose objective is one pairwise leaf (n <= 128 terms) of
+// position-local terms (f1, f2, f4, f5, f6, f9 and the probe): C1-C4.
+//
+// "Chain mapping": 8 consecutive lanes own one particle; lane k holds the
+// positions j = k + 8m (m < M) in registers -- exactly the elements numpy's
+// accumulator r[k] sums, in the same order -- so the whole iteration is
+// register-resident and barrier-free:
+//   load X, P (j = k + 8m)  -> keyed draw + select -> stream new X to HBM
+//   -> term(j) -> r[k] += term in order -> xor-shuffle combine (numpy's
+//   ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7))) -> tail terms summed in order
+//   -> fitness (identical on the 8 lanes) -> pbest <= test -> improved rows
+//   written to P from registers.
+// A warp runs 4 particles at a time, persistent over the swarm; no shared
+// memory beyond the CTA's gbest copy, no __syncthreads in the loop.
+// f4's neighbour x[j+1] comes from lane k+1 (same m) or, for k = 7, from
+// lane 0 at m+1, with a single shuffle (lane 0 provides x[m+1]).
+template <int FN>
+__host__ __device__ constexpr bool chain_fn() {
+  return FN == 0 || FN == 1 || FN == 2 || FN == 4 || FN == 5 || FN == 6 || FN == 9;
+}
+
+template <typename T, int FN>
+__device__ __forceinline__ T chain_term1(T x, T nb, int e) {
+  using N = Num<T>;
+  if constexpr (FN == 2) {
+    return N::mul(N::mul((T)(e + 1), x), x);
+  } else if constexpr (FN == 4) {
+    const T d = N::sub(nb, N::mul(x, x));
+    const T o = N::sub((T)1, x);
+    return N::add(N::mul(N::mul((T)100, d), d), N::mul(o, o));
+  } else if constexpr (FN == 5) {
+    return N::sub(N::mul(x, x), N::mul((T)10, N::cos_(N::mul((T)N::TWO_PI, x))));
+  } else if constexpr (FN == 9) {
+    return N::mul(x, N::sin_(N::sqrt_(fabs(x))));
+  } else {  // 0, 1, 6
+    return N::mul(x, x);
+  }
+}
+
+#ifndef PSSO_CHAIN_NT
+#define PSSO_CHAIN_NT 256
+#endif
+#ifndef PSSO_CHAIN_MINB
+#define PSSO_CHAIN_MINB 2
+#endif
+
+template <typename T, int FN, int RNG, int M, bool INIT>
+__global__ void __launch_bounds__(PSSO_CHAIN_NT, PSSO_CHAIN_MINB)
+    k_chain(const __grid_constant__ TileParams p) {
+  using N = Num<T>;
+  constexpr int NTC = PSSO_CHAIN_NT;
+  constexpr int NW = NTC / 32;
+  extern __shared__ __align__(16) unsigned char smem[];
+  T* gb = reinterpret_cast<T*>(smem);
+  double* red_f = reinterpret_cast<double*>(smem + p.off_red);
+  int64_t* red_i = reinterpret_cast<int64_t*>(smem + p.off_red + 8 * NW);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int k = lane & 7;
+  const int seg = lane & ~7;  // first lane of this particle's 8-lane segment
+  const int D = p.D;
+  const int mode = INIT ? (M_INIT | M_EVAL | M_CAND | M_SOLF)
+                        : (M_SEARCH | M_EVAL | M_PBEST | M_CAND | (p.mode & M_SOLF));
+  if (!INIT && p.bad && *(volatile unsigned long long*)p.bad != ~0ull) return;
+  const int64_t t = p.t_dev ? *p.t_dev : p.t_arg;
+  T* __restrict__ X = reinterpret_cast<T*>(p.X);
+  T* __restrict__ P = reinterpret_cast<T*>(p.P);
+
+  uint64_t rootb = 0, rootf = 0;
+  if constexpr (RNG == 0) {
+    if (INIT) {
+      rootb = root64(p.seed, STREAM_INIT, 0);
+    } else {
+      rootb = root64(p.seed, STREAM_BRANCH, (uint64_t)t);
+      rootf = root64(p.seed, STREAM_FRESH, (uint64_t)t);
+    }
+  }
+  if (!INIT) {
+    const T* g = reinterpret_cast<const T*>(p.gbest);
+    for (int j = tid; j < D; j += NTC) gb[j] = g[j];
+    __syncthreads();
+  }
+
+  const int n = p.plan.n;                 // terms (single leaf, n <= 128)
+  const int mlen = n >= 8 ? (n >> 3) : 0;  // chain length
+  const int tail = n - 8 * mlen;           // tail terms, at m = mlen, lanes 0..tail-1
+  const uint64_t gam0 = GAMMA * (uint64_t)(k + 1);
+  const uint64_t gstep = GAMMA * 8ull;
+  const int64_t rows = p.rows;
+  const int64_t ngroups = (rows + 3) >> 2;
+  double best_f = CUDART_INF;
+  int64_t best_i = INT64_MAX;
+
+  for (int64_t grp = (int64_t)blockIdx.x * NW + warp; grp < ngroups;
+       grp += (int64_t)gridDim.x * NW) {
+    const int64_t r = 4 * grp + (lane >> 3);
+    const bool rv = r < rows;
+    const int64_t gi = p.row_lo + r;
+    T* xr = X + r * (int64_t)D;
+    T* pr = P + r * (int64_t)D;
+    double pf_row = 0.0;
+    if (!INIT && rv) pf_row = p.p_f[r];
+
+    T x[M];
+    T pv[M];
+    if (!INIT) {
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        const int j = k + 8 * m;
+        if (rv && j < D) {
+          x[m] = ldg_stream<T, 1>(xr + j).v[0];
+          pv[m] = ldg_stream<T, 1>(pr + j).v[0];
+        } else {
+          x[m] = (T)0;
+          pv[m] = (T)0;
+        }
+      }
+    }
+    uint64_t hb = 0, hf = 0;
+    if constexpr (RNG == 0) {
+      hb = fold64(rootb, (uint64_t)gi);
+      if (!INIT) hf = fold64(rootf, (uint64_t)gi);
+    }
+
+    // ---- positions
+    uint64_t g = gam0;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const int j = k + 8 * m;
+      if (rv && j < D) {
+        T v;
+        if constexpr (INIT) {
+          uint64_t h;
+          if constexpr (RNG == 0) {
+            h = mix64(hb ^ g);
+          } else {
+            Philox4 w = philox4x32_10((uint32_t)(j >> 1), (uint32_t)gi, (uint32_t)(gi >> 32),
+                                      0xFFFFFFFFu, (uint32_t)p.seed, (uint32_t)(p.seed >> 32));
+            const int s2 = (j & 1) * 2;
+            h = ((uint64_t)w.w[s2] << 32) | w.w[s2 + 1];
+          }
+          v = (T)__dadd_rn(p.var_min, __dmul_rn(p.span, unit53(h)));
+          stg_stream<T, 1>(pr + j, VecT<T, 1>{{v}});
+        } else {
+          if constexpr (RNG == 0) {  // core.py:138-173, branch-free (see search_chunk)
+            const uint64_t kb = mix64(hb ^ g) >> 11;
+            const double fresh = __dadd_rn(p.var_min, __dmul_rn(p.span, unit53(mix64(hf ^ g))));
+            v = x[m];
+            v = kb >= p.Kw ? pv[m] : v;
+            v = kb >= p.Kp ? gb[j] : v;
+            v = kb >= p.Kg ? (T)fresh : v;
+          } else {
+            VecT<T, 1> xv{{x[m]}}, pb{{pv[m]}}, gv{{gb[j]}};
+            v = search_chunk<T, 1, 1>(p, xv, pb, gv, 0, 0, j, (uint64_t)gi, t).v[0];
+          }
+        }
+        x[m] = v;
+        stg_stream<T, 1>(xr + j, VecT<T, 1>{{v}});
+      }
+      g += gstep;
+    }
+
+    // ---- fitness: lane k accumulates terms k, k+8, ... in order
+    T a1 = (T)0, a2 = (T)0, t1 = (T)0, t2 = (T)0;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const int e = k + 8 * m;
+      T nb = (T)0;
+      if constexpr (FN == 4) {
+        const T nxt = (m + 1 < M) ? x[m + 1 < M ? m + 1 : m] : (T)0;
+        const T prov = (k == 0) ? nxt : x[m];
+        nb = __shfl_sync(0xffffffffu, prov, k < 7 ? lane + 1 : lane - 7);
+      }
+      if (m < mlen || (m == mlen && k < tail)) {
+        const T v1 = chain_term1<T, FN>(x[m], nb, e);
+        T v2 = (T)0;
+        if constexpr (two_sums(FN)) v2 = N::cos_(N::mul((T)N::TWO_PI, x[m]));
+        if (m < mlen) {
+          a1 = (m == 0) ? v1 : N::add(a1, v1);
+          if constexpr (two_sums(FN)) a2 = (m == 0) ? v2 : N::add(a2, v2);
+        } else {
+          t1 = v1;
+          t2 = v2;
+        }
+      }
+    }
+    a1 = N::add(a1, __shfl_xor_sync(0xffffffffu, a1, 1));
+    a1 = N::add(a1, __shfl_xor_sync(0xffffffffu, a1, 2));
+    a1 = N::add(a1, __shfl_xor_sync(0xffffffffu, a1, 4));
+    if constexpr (two_sums(FN)) {
+      a2 = N::add(a2, __shfl_xor_sync(0xffffffffu, a2, 1));
+      a2 = N::add(a2, __shfl_xor_sync(0xffffffffu, a2, 2));
+      a2 = N::add(a2, __shfl_xor_sync(0xffffffffu, a2, 4));
+    }
+    T s1 = mlen > 0 ? a1 : (T)0;
+    T s2 = mlen > 0 ? a2 : (T)0;
+    for (int q = 0; q < tail; ++q) {  // numpy adds the tail left to right
+      s1 = N::add(s1, __shfl_sync(0xffffffffu, t1, seg + q));
+      if constexpr (two_sums(FN)) s2 = N::add(s2, __shfl_sync(0xffffffffu, t2, seg + q));
+    }
+    const T x0 = __shfl_sync(0xffffffffu, x[0], seg);
+    const double f = finish<T, FN>(s1, s2, (T)1, D, &x0, p.probe_level);
+
+    // ---- bookkeeping (identical on the 8 lanes; lane k == 0 writes)
+    if (rv) {
+      if (k == 0) {
+        if (!isfinite(f) && p.bad)
+          atomicMin(p.bad, ((unsigned long long)(t + 1) << 40) | (unsigned long long)gi);
+        if (p.sol_f && ((mode & M_SOLF) || !isfinite(f))) p.sol_f[r] = f;
+      }
+      double pf = f;
+      if (INIT) {
+        if (k == 0) p.p_f[r] = f;
+      } else {
+        const bool imp = f <= pf_row;  // parallel.py:109, ties refresh
+        pf = imp ? f : pf_row;
+        if (imp) {
+          if (k == 0) p.p_f[r] = f;
+#pragma unroll
+          for (int m = 0; m < M; ++m) {
+            const int j = k + 8 * m;
+            if (j < D) stg_stream<T, 1>(pr + j, VecT<T, 1>{{x[m]}});
+          }
+        }
+      }
+      if (k == 0 && lex_less(pf, gi, best_f, best_i)) { best_f = pf; best_i = gi; }
+    }
+  }
+
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double of = __shfl_xor_sync(0xffffffffu, best_f, o);
+    const int64_t oi = __shfl_xor_sync(0xffffffffu, best_i, o);
+    if (lex_less(of, oi, best_f, best_i)) { best_f = of; best_i = oi; }
+  }
+  if (lane == 0) { red_f[warp] = best_f; red_i[warp] = best_i; }
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < NW; ++w)
+      if (lex_less(red_f[w], red_i[w], best_f, best_i)) { best_f = red_f[w]; best_i = red_i[w]; }
+    p.slot_f[blockIdx.x] = best_f;
+    p.slot_i[blockIdx.x] = best_i;
   }
 }
 
