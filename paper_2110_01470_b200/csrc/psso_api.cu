@@ -424,6 +424,7 @@ TileParams tile_params(psso_ctx* c, int mode, int64_t t, const int64_t* t_dev, b
   p.Kw32 = c->Kw32; p.Kp32 = c->Kp32; p.Kg32 = c->Kg32;
   p.var_min = c->cfg.var_min;
   p.span = c->cfg.var_max - c->cfg.var_min;
+  p.span53 = std::ldexp(p.span, -53);
   p.probe_level = c->cfg.probe_level;
   p.t_arg = t;
   p.t_dev = t_dev;
@@ -559,16 +560,21 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
     const int64_t D = cfg->nvar;
     const int M = D <= 32 ? 4 : D <= 64 ? 8 : D <= 128 ? 16 : 0;
     const char* off = std::getenv("PSSO_NO_CHAIN");
-    if (M && terms_of(cfg->fn_id, D) <= 128 && !(off && *off && *off != '0')) {
-      const void* f = chain_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, M, false);
-      const void* i = chain_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, M, true);
+    // the chain kernel's branch-free trig (psso_trig.cuh) is valid for
+    // positions in a box of moderate size; wider boxes take the tile kernels
+    const double box = std::max(std::fabs(cfg->var_min), std::fabs(cfg->var_max));
+    const bool trig_ok = box <= (cfg->dtype == PSSO_F64 ? kChainTrigMaxAbs : 1.0e6);
+    if (M && terms_of(cfg->fn_id, D) <= 128 && trig_ok && !(off && *off && *off != '0')) {
+      const bool full = D == 8 * M;
+      const void* f = chain_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, M, false, full);
+      const void* i = chain_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, M, true, false);
       if (f && i) {
         c->fused_fn = f;
         c->init_fn = i;
         c->chain = true;
         const int es = cfg->dtype == PSSO_F64 ? 8 : 4;
         c->LF.off_red = (int)align16((size_t)D * es);
-        c->LF.smem = (size_t)c->LF.off_red + 128;
+        c->LF.smem = (size_t)c->LF.off_red + 128 + 64 * M;  // reduction + xs30(gamma*(j+1)) table
       }
     }
   }

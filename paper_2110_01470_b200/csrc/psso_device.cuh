@@ -19,6 +19,8 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
+#include "psso_trig.cuh"
+
 namespace psso {
 
 constexpr int NT = 256;            // threads per CTA of k_tile
@@ -92,6 +94,7 @@ struct TileParams {
   uint64_t Kw, Kp, Kg;         // reference mode: branch k = h >> 11 compared < K
   uint64_t Kw32, Kp32, Kg32;   // philox mode: 32-bit word compared < K32
   double var_min, span;
+  double span53;               // span * 2^-53 (fresh = var_min + k * span53, exact rescale)
   double probe_level;
   int64_t t_arg;
   const int64_t* t_dev;        // if non-null, the iteration is read from here
@@ -111,6 +114,13 @@ struct TileParams {
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {  // rng.py:48-52
   z = (z ^ (z >> 30)) * MIX1;
+  z = (z ^ (z >> 27)) * MIX2;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint64_t xs30(uint64_t z) { return z ^ (z >> 30); }
+// mix64 after its first xorshift: mix64(z) == mix64_tail(xs30(z))
+__device__ __forceinline__ uint64_t mix64_tail(uint64_t z) {
+  z *= MIX1;
   z = (z ^ (z >> 27)) * MIX2;
   return z ^ (z >> 31);
 }
@@ -944,10 +954,14 @@ __device__ __forceinline__ T chain_term1(T x, T nb, int e) {
     const T d = N::sub(nb, N::mul(x, x));
     const T o = N::sub((T)1, x);
     return N::add(N::mul(N::mul((T)100, d), d), N::mul(o, o));
-  } else if constexpr (FN == 5) {
-    return N::sub(N::mul(x, x), N::mul((T)10, N::cos_(N::mul((T)N::TWO_PI, x))));
+  } else if constexpr (FN == 5) {  // x*x - 10*cos(2*pi*x) as x*x + (-+10)*|cos|
+    uint32_t odd;
+    const T p = Trig<T>::cos2pi_abs(x, odd);
+    const T c = Trig<T>::flip((T)-10, odd);
+    if constexpr (sizeof(T) == 8) return __fma_rn(p, c, N::mul(x, x));
+    else return __fmaf_rn(p, c, N::mul(x, x));
   } else if constexpr (FN == 9) {
-    return N::mul(x, N::sin_(N::sqrt_(fabs(x))));
+    return N::mul(x, Trig<T>::sin_(N::sqrt_(fabs(x))));
   } else {  // 0, 1, 6
     return N::mul(x, x);
   }
@@ -960,7 +974,7 @@ __device__ __forceinline__ T chain_term1(T x, T nb, int e) {
 #define PSSO_CHAIN_MINB 2
 #endif
 
-template <typename T, int FN, int RNG, int M, bool INIT>
+template <typename T, int FN, int RNG, int M, bool INIT, bool FULL>
 __global__ void __launch_bounds__(PSSO_CHAIN_NT, PSSO_CHAIN_MINB)
     k_chain(const __grid_constant__ TileParams p) {
   using N = Num<T>;
@@ -991,13 +1005,17 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, PSSO_CHAIN_MINB)
       rootf = root64(p.seed, STREAM_FRESH, (uint64_t)t);
     }
   }
+  uint64_t* xg = reinterpret_cast<uint64_t*>(smem + p.off_red + 16 * NW);  // [M][8]
   if (!INIT) {
     const T* g = reinterpret_cast<const T*>(p.gbest);
     for (int j = tid; j < D; j += NTC) gb[j] = g[j];
+    for (int q = tid; q < 8 * M; q += NTC) xg[q] = xs30(GAMMA * (uint64_t)(q + 1));  // q = j
     __syncthreads();
   }
 
-  const int n = p.plan.n;                 // terms (single leaf, n <= 128)
+  // FULL: D == 8*M, so the chain lengths and the tail are compile-time
+  // (f4 has D-1 terms: M-1 full chains and a 7-term tail)
+  const int n = FULL ? (FN == 4 ? 8 * M - 1 : 8 * M) : p.plan.n;  // terms (one leaf, <= 128)
   const int mlen = n >= 8 ? (n >> 3) : 0;  // chain length
   const int tail = n - 8 * mlen;           // tail terms, at m = mlen, lanes 0..tail-1
   const uint64_t gam0 = GAMMA * (uint64_t)(k + 1);
@@ -1012,20 +1030,24 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, PSSO_CHAIN_MINB)
     const int64_t r = 4 * grp + (lane >> 3);
     const bool rv = r < rows;
     const int64_t gi = p.row_lo + r;
+    // rows past the end (last group only) compute on a clamped row and store nothing
+    const int64_t rl = rv ? r : rows - 1;
     T* xr = X + r * (int64_t)D;
     T* pr = P + r * (int64_t)D;
     double pf_row = 0.0;
-    if (!INIT && rv) pf_row = p.p_f[r];
+    if (!INIT) pf_row = p.p_f[rl];
 
     T x[M];
     T pv[M];
     if (!INIT) {
+      const T* xl = X + rl * (int64_t)D;
+      const T* pl = P + rl * (int64_t)D;
 #pragma unroll
       for (int m = 0; m < M; ++m) {
         const int j = k + 8 * m;
-        if (rv && j < D) {
-          x[m] = ldg_stream<T, 1>(xr + j).v[0];
-          pv[m] = ldg_stream<T, 1>(pr + j).v[0];
+        if (FULL || j < D) {
+          x[m] = ldg_stream<T, 1>(xl + j).v[0];
+          pv[m] = ldg_stream<T, 1>(pl + j).v[0];
         } else {
           x[m] = (T)0;
           pv[m] = (T)0;
@@ -1039,13 +1061,12 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, PSSO_CHAIN_MINB)
     }
 
     // ---- positions
-    uint64_t g = gam0;
+    if constexpr (INIT) {
+      uint64_t g = gam0;
 #pragma unroll
-    for (int m = 0; m < M; ++m) {
-      const int j = k + 8 * m;
-      if (rv && j < D) {
-        T v;
-        if constexpr (INIT) {
+      for (int m = 0; m < M; ++m) {
+        const int j = k + 8 * m;
+        if (rv && (FULL || j < D)) {
           uint64_t h;
           if constexpr (RNG == 0) {
             h = mix64(hb ^ g);
@@ -1055,25 +1076,38 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, PSSO_CHAIN_MINB)
             const int s2 = (j & 1) * 2;
             h = ((uint64_t)w.w[s2] << 32) | w.w[s2 + 1];
           }
-          v = (T)__dadd_rn(p.var_min, __dmul_rn(p.span, unit53(h)));
+          const T v = (T)__dadd_rn(p.var_min, __dmul_rn(p.span, unit53(h)));
           stg_stream<T, 1>(pr + j, VecT<T, 1>{{v}});
+          x[m] = v;
+          stg_stream<T, 1>(xr + j, VecT<T, 1>{{v}});
+        }
+        g += gstep;
+      }
+    } else {
+      // core.py:138-173, branch-free (see search_chunk).  Reference RNG:
+      // mix64(h ^ g) = mix64_tail(xs30(h) ^ xs30(g)) since the first
+      // xorshift is linear over xor; xs30(g_j) comes from the CTA's table.
+      const uint64_t xb = xs30(hb), xf = xs30(hf);
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        const int j = k + 8 * m;
+        T v;
+        if constexpr (RNG == 0) {
+          const uint64_t gx = xg[m * 8 + k];
+          const uint64_t kb = mix64_tail(xb ^ gx) >> 11;
+          const double fresh =
+              __dadd_rn(p.var_min, __dmul_rn(p.span53, (double)(mix64_tail(xf ^ gx) >> 11)));
+          v = x[m];
+          v = kb >= p.Kw ? pv[m] : v;
+          v = kb >= p.Kp ? gb[j] : v;
+          v = kb >= p.Kg ? (T)fresh : v;
         } else {
-          if constexpr (RNG == 0) {  // core.py:138-173, branch-free (see search_chunk)
-            const uint64_t kb = mix64(hb ^ g) >> 11;
-            const double fresh = __dadd_rn(p.var_min, __dmul_rn(p.span, unit53(mix64(hf ^ g))));
-            v = x[m];
-            v = kb >= p.Kw ? pv[m] : v;
-            v = kb >= p.Kp ? gb[j] : v;
-            v = kb >= p.Kg ? (T)fresh : v;
-          } else {
-            VecT<T, 1> xv{{x[m]}}, pb{{pv[m]}}, gv{{gb[j]}};
-            v = search_chunk<T, 1, 1>(p, xv, pb, gv, 0, 0, j, (uint64_t)gi, t).v[0];
-          }
+          VecT<T, 1> xv{{x[m]}}, pb{{pv[m]}}, gv{{gb[j]}};
+          v = search_chunk<T, 1, 1>(p, xv, pb, gv, 0, 0, j, (uint64_t)gi, t).v[0];
         }
         x[m] = v;
-        stg_stream<T, 1>(xr + j, VecT<T, 1>{{v}});
+        if (rv && (FULL || j < D)) stg_stream<T, 1>(xr + j, VecT<T, 1>{{v}});
       }
-      g += gstep;
     }
 
     // ---- fitness: lane k accumulates terms k, k+8, ... in order
@@ -1090,7 +1124,7 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, PSSO_CHAIN_MINB)
       if (m < mlen || (m == mlen && k < tail)) {
         const T v1 = chain_term1<T, FN>(x[m], nb, e);
         T v2 = (T)0;
-        if constexpr (two_sums(FN)) v2 = N::cos_(N::mul((T)N::TWO_PI, x[m]));
+        if constexpr (two_sums(FN)) v2 = Trig<T>::cos2pi(x[m]);
         if (m < mlen) {
           a1 = (m == 0) ? v1 : N::add(a1, v1);
           if constexpr (two_sums(FN)) a2 = (m == 0) ? v2 : N::add(a2, v2);
@@ -1135,7 +1169,7 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, PSSO_CHAIN_MINB)
 #pragma unroll
           for (int m = 0; m < M; ++m) {
             const int j = k + 8 * m;
-            if (j < D) stg_stream<T, 1>(pr + j, VecT<T, 1>{{x[m]}});
+            if (FULL || j < D) stg_stream<T, 1>(pr + j, VecT<T, 1>{{x[m]}});
           }
         }
       }

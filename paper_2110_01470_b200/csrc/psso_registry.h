@@ -1,4 +1,4 @@
-// psso_registry.h -- lookup of the k_tile template instantiations, which are
+// psso_registry.h -- lookup of the k_tile / k_fused / k_chain template instantiations, which are
 // compiled in separate translation units (psso_tiles_*.cu) to build in parallel.
 #pragma once
 
@@ -8,15 +8,15 @@ const void* tile_kernel_f64_philox(int fn, int vec, bool fused);
 const void* tile_kernel_f32_ref(int fn, int vec, bool fused);
 const void* tile_kernel_f32_philox(int fn, int vec, bool fused);
 
-const void* chain_kernel_f64_ref(int fn, int m, bool init);
-const void* chain_kernel_f64_philox(int fn, int m, bool init);
-const void* chain_kernel_f32_ref(int fn, int m, bool init);
-const void* chain_kernel_f32_philox(int fn, int m, bool init);
+const void* chain_kernel_f64_ref(int fn, int m, bool init, bool full);
+const void* chain_kernel_f64_philox(int fn, int m, bool init, bool full);
+const void* chain_kernel_f32_ref(int fn, int m, bool init, bool full);
+const void* chain_kernel_f32_philox(int fn, int m, bool init, bool full);
 
-inline const void* chain_kernel(int dtype, int rng, int fn, int m, bool init) {
+inline const void* chain_kernel(int dtype, int rng, int fn, int m, bool init, bool full) {
   if (dtype == 0)
-    return rng == 0 ? chain_kernel_f64_ref(fn, m, init) : chain_kernel_f64_philox(fn, m, init);
-  return rng == 0 ? chain_kernel_f32_ref(fn, m, init) : chain_kernel_f32_philox(fn, m, init);
+    return rng == 0 ? chain_kernel_f64_ref(fn, m, init, full) : chain_kernel_f64_philox(fn, m, init, full);
+  return rng == 0 ? chain_kernel_f32_ref(fn, m, init, full) : chain_kernel_f32_philox(fn, m, init, full);
 }
 
 inline const void* tile_kernel(int dtype, int rng, int fn, int vec, bool fused) {
