@@ -342,6 +342,7 @@ struct psso_ctx {
   int grid;
   int fused_grid;
   int init_grid;
+  size_t init_smem;      // dynamic smem of the chain init kernel (no prefetch buffers)
   int argmin_grid;
   int nslots;
   double* slot_f;
@@ -573,8 +574,15 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
         c->init_fn = i;
         c->chain = true;
         const int es = cfg->dtype == PSSO_F64 ? 8 : 4;
+        // gbest | warp reduction + xs30(gamma*(j+1)) table | per-warp mbarriers |
+        // per-warp prefetch buffers (FULL iteration kernel, psso_device.cuh)
+        const int nw = PSSO_CHAIN_NT / 32;
         c->LF.off_red = (int)align16((size_t)D * es);
-        c->LF.smem = (size_t)c->LF.off_red + 128 + 64 * M;  // reduction + xs30(gamma*(j+1)) table
+        c->LF.off_bar = (int)align16((size_t)c->LF.off_red + 128 + 64 * M);
+        c->LF.off_xs = (int)((c->LF.off_bar + 8 * nw + 127) & ~127);
+        c->LF.smem = full && PSSO_CHAIN_PF ? (size_t)c->LF.off_xs + (size_t)nw * 8 * (8 * M + 8) * es
+                                           : (size_t)c->LF.off_bar;
+        c->init_smem = (size_t)c->LF.off_bar;
       }
     }
   }
@@ -605,7 +613,7 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
   c->init_grid = c->grid;
   if (c->chain) {  // 4 particles per warp, 8 warps per CTA
     int per_sm_init = 0;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_init, c->init_fn, NT, c->LF.smem)) != cudaSuccess ||
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_init, c->init_fn, NT, c->init_smem)) != cudaSuccess ||
         per_sm_init < 1) {
       delete c;
       return e != cudaSuccess ? cuda_fail(nullptr, e, "occupancy") : fail(nullptr, PSSO_E_UNSUPPORTED, "chain kernel cannot be resident");
@@ -673,7 +681,7 @@ static int launch_init(psso_ctx* c) {
   if (!c->chain) return launch_tile(c, tile_params(c, M_INIT | M_EVAL | M_CAND | M_SOLF, -1, nullptr));
   TileParams p = tile_params(c, M_INIT | M_EVAL | M_CAND | M_SOLF, -1, nullptr, true);
   void* args[] = {(void*)&p};
-  CK(c, cudaLaunchKernel(c->init_fn, dim3(c->init_grid), dim3(NT), args, c->LF.smem, c->stream));
+  CK(c, cudaLaunchKernel(c->init_fn, dim3(c->init_grid), dim3(NT), args, c->init_smem, c->stream));
   c->launches++;
   return PSSO_OK;
 }

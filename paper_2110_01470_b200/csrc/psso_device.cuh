@@ -973,6 +973,15 @@ __device__ __forceinline__ T chain_term1(T x, T nb, int e) {
 #ifndef PSSO_CHAIN_MINB
 #define PSSO_CHAIN_MINB 2
 #endif
+#ifndef PSSO_CHAIN_PF
+#define PSSO_CHAIN_PF 1  // FULL iteration kernel: TMA prefetch of the next group
+#endif
+
+// Shared-memory row stride of the chain kernel's per-warp prefetch buffer:
+// rows padded by 8 elements so the four 8-lane segments of a warp read
+// disjoint banks (fp64: two wavefronts per LDS.64, fp32: one per LDS.32).
+template <typename T, int M>
+__host__ __device__ constexpr int chain_row_stride() { return (8 * M + 8) * (int)sizeof(T); }
 
 template <typename T, int FN, int RNG, int M, bool INIT, bool FULL>
 __global__ void __launch_bounds__(PSSO_CHAIN_NT, PSSO_CHAIN_MINB)
@@ -1025,8 +1034,37 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, PSSO_CHAIN_MINB)
   double best_f = CUDART_INF;
   int64_t best_i = INT64_MAX;
 
-  for (int64_t grp = (int64_t)blockIdx.x * NW + warp; grp < ngroups;
-       grp += (int64_t)gridDim.x * NW) {
+  // PF: each warp streams its next group of 4 rows (X and P) into a private
+  // shared-memory buffer with TMA bulk copies while it computes the current
+  // group from registers, so HBM reads overlap the hash/select/fitness work
+  // without costing registers.  Lanes 0..7 each copy one row of X or P.
+  constexpr bool PF = FULL && !INIT && PSSO_CHAIN_PF;
+  constexpr int RS = chain_row_stride<T, M>();
+  uint64_t* wbar = reinterpret_cast<uint64_t*>(smem + p.off_bar) + warp;
+  unsigned char* wbuf = smem + p.off_xs + (size_t)warp * (8 * RS);
+  const int64_t gstride = (int64_t)gridDim.x * NW;
+  uint32_t wphase = 0;
+  auto prefetch = [&](int64_t g) {  // whole warp calls; lanes 0..7 issue
+    if (g >= ngroups) return;
+    const int nr = (int)min((int64_t)4, rows - 4 * g);
+    if (lane == 0) mbar_expect_tx(wbar, (uint32_t)(2 * nr * 8 * M * sizeof(T)));
+    __syncwarp();
+    const int s = lane & 3;
+    if (lane < 8 && s < nr) {
+      const T* src = (lane < 4 ? X : P) + (4 * g + s) * (int64_t)(8 * M);
+      bulk_g2s(wbuf + (lane >> 2) * 4 * RS + s * RS, src, (uint32_t)(8 * M * sizeof(T)), wbar);
+    }
+  };
+  if constexpr (PF) {
+    if (lane == 0) {
+      mbar_init(wbar, 1);
+      mbar_fence_init();
+    }
+    __syncwarp();
+    prefetch((int64_t)blockIdx.x * NW + warp);
+  }
+
+  for (int64_t grp = (int64_t)blockIdx.x * NW + warp; grp < ngroups; grp += gstride) {
     const int64_t r = 4 * grp + (lane >> 3);
     const bool rv = r < rows;
     const int64_t gi = p.row_lo + r;
@@ -1039,7 +1077,21 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, PSSO_CHAIN_MINB)
 
     T x[M];
     T pv[M];
-    if (!INIT) {
+    if constexpr (PF) {
+      mbar_wait(wbar, wphase);
+      wphase ^= 1;
+      const int sr = (int)(rl - 4 * grp);  // clamped row within the group
+      const T* xs = reinterpret_cast<const T*>(wbuf + sr * RS);
+      const T* ps = reinterpret_cast<const T*>(wbuf + 4 * RS + sr * RS);
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        x[m] = xs[k + 8 * m];
+        pv[m] = ps[k + 8 * m];
+      }
+      __syncwarp();  // the whole buffer is in registers before it is refilled
+      fence_proxy_async();
+      prefetch(grp + gstride);
+    } else if (!INIT) {
       const T* xl = X + rl * (int64_t)D;
       const T* pl = P + rl * (int64_t)D;
 #pragma unroll
