@@ -339,6 +339,7 @@ struct psso_ctx {
   const void* fused_fn;  // fused iteration kernel (the hot path)
   const void* init_fn;   // initialization kernel (k_chain<INIT> or k_tile)
   bool chain;            // fused/init run the register-resident chain kernel
+  int rows_w;            // >0: the fused iteration is k_rows with W = rows_w warps per row
   int grid;
   int fused_grid;
   int init_grid;
@@ -586,6 +587,28 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
       }
     }
   }
+  c->rows_w = 0;
+  {  // long rows (C5): D = 512*W, a balanced tree of 4W leaves -> k_rows
+    const int64_t D = cfg->nvar;
+    const int W = D == 512 ? 1 : D == 1024 ? 2 : D == 2048 ? 4 : D == 4096 ? 8 : 0;
+    const char* off = std::getenv("PSSO_NO_ROWS");
+    const double box = std::max(std::fabs(cfg->var_min), std::fabs(cfg->var_max));
+    const bool trig_ok = box <= (cfg->dtype == PSSO_F64 ? kChainTrigMaxAbs : 1.0e6);
+    const void* f = W && trig_ok && !(off && *off && *off != '0')
+                        ? rows_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, W) : nullptr;
+    if (f) {
+      c->fused_fn = f;
+      c->rows_w = W;
+      const int es = cfg->dtype == PSSO_F64 ? 8 : 4;
+      // gbest | warp reduction | leaf values [8/W][2][4W] | flags | mbarriers | prefetch buffers
+      c->LF.off_red = (int)align16((size_t)D * es);
+      c->LF.off_leaf = c->LF.off_red + 128;
+      c->LF.off_flag = c->LF.off_leaf + 512;
+      c->LF.off_bar = (int)align16((size_t)c->LF.off_flag + 32);
+      c->LF.off_xs = (int)((c->LF.off_bar + 64 + 127) & ~127);
+      c->LF.smem = (size_t)c->LF.off_xs + 8 * 8 * (size_t)(128 + 8) * es;
+    }
+  }
   if (!c->tile_fn || !c->fused_fn) {
     delete c;
     return fail(nullptr, PSSO_E_UNSUPPORTED, "no kernel instantiation for this configuration");
@@ -621,6 +644,10 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
     const int64_t nctas = (rows + 4 * (NT / 32) - 1) / (4 * (NT / 32));
     c->fused_grid = (int)std::min<int64_t>(nctas, (int64_t)per_sm_fused * c->num_sms);
     c->init_grid = (int)std::min<int64_t>(nctas, (int64_t)per_sm_init * c->num_sms);
+  }
+  if (c->rows_w) {  // 8 / W rows per CTA round
+    const int rpc = 8 / c->rows_w;
+    c->fused_grid = (int)std::min<int64_t>((rows + rpc - 1) / rpc, (int64_t)per_sm_fused * c->num_sms);
   }
   c->argmin_grid = (int)std::min<int64_t>((rows + 255) / 256, 4 * c->num_sms);
   c->nslots = std::max(std::max(std::max(c->grid, c->fused_grid), c->init_grid), c->argmin_grid);

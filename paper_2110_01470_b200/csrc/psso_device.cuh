@@ -1245,4 +1245,200 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, PSSO_CHAIN_MINB)
   }
 }
 
+// ---------------------------------------------------------------- k_rows ----
+// Hot path for long rows (C5: D = 4096): D = 512*W, W in {1, 2, 4, 8}, whose
+// numpy reduction is a balanced pairwise tree of 4W leaves of 128 terms
+// (add.reduce splits at n/2, a multiple of 8, down to 128).  Each row is
+// owned by W warps of one CTA (8/W rows per CTA round); warp slice sw holds
+// leaves 4sw..4sw+3, one per 8-lane segment, with the chain mapping of
+// k_chain inside the leaf (lane k: j = 128*leaf + k + 8m, m < 16), so the
+// positions of the whole row stay in registers until the pBest decision:
+//   TMA-prefetched X/P slice -> keyed draw + select -> X streamed to HBM ->
+//   leaf chains + xor-shuffle combine -> leaf values to smem -> one warp per
+//   row combines the 4W leaves with a butterfly (xor 1, 2, ..., 2W: exactly
+//   the balanced tree, fp add being commutative) -> fitness, `<=`, p_f ->
+//   improved rows written to P from registers by all W warps.
+// Two CTA barriers per round; no atomics.  Objectives with position-local
+// terms (f1, f2, f5, f6, f9, probe).
+template <int FN>
+__host__ __device__ constexpr bool rows_fn() {
+  return FN == 0 || FN == 1 || FN == 2 || FN == 5 || FN == 6 || FN == 9;
+}
+
+template <typename T, int FN, int RNG, int W>
+__global__ void __launch_bounds__(256, 2) k_rows(const __grid_constant__ TileParams p) {
+  using N = Num<T>;
+  constexpr int NW = 8, RPC = NW / W, M = 16, D = 512 * W, NL = 4 * W;
+  constexpr int RS = chain_row_stride<T, M>();
+  extern __shared__ __align__(128) unsigned char smem[];
+  T* gb = reinterpret_cast<T*>(smem);
+  double* red_f = reinterpret_cast<double*>(smem + p.off_red);
+  int64_t* red_i = reinterpret_cast<int64_t*>(smem + p.off_red + 8 * NW);
+  double* leafv = reinterpret_cast<double*>(smem + p.off_leaf);  // [RPC][2][NL]
+  int* flag = reinterpret_cast<int*>(smem + p.off_flag);          // [RPC]
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int k = lane & 7, s = lane >> 3;
+  const int slot = warp / W, sw = warp % W;
+  const int mode = M_SEARCH | M_EVAL | M_PBEST | M_CAND | (p.mode & M_SOLF);
+  if (p.bad && *(volatile unsigned long long*)p.bad != ~0ull) return;
+  const int64_t t = p.t_dev ? *p.t_dev : p.t_arg;
+  T* __restrict__ X = reinterpret_cast<T*>(p.X);
+  T* __restrict__ P = reinterpret_cast<T*>(p.P);
+
+  uint64_t rootb = 0, rootf = 0;
+  if constexpr (RNG == 0) {
+    rootb = root64(p.seed, STREAM_BRANCH, (uint64_t)t);
+    rootf = root64(p.seed, STREAM_FRESH, (uint64_t)t);
+  }
+  {
+    const T* g = reinterpret_cast<const T*>(p.gbest);
+    for (int j = tid; j < D; j += 256) gb[j] = g[j];
+  }
+  const int jb = 512 * sw + 128 * s + k;  // this lane's first element; j = jb + 8m
+  const uint64_t g0 = GAMMA * (uint64_t)(jb + 1);
+
+  const int64_t rows = p.rows;
+  const int64_t rstride = (int64_t)gridDim.x * RPC;
+  uint64_t* wbar = reinterpret_cast<uint64_t*>(smem + p.off_bar) + warp;
+  unsigned char* wbuf = smem + p.off_xs + (size_t)warp * (8 * RS);
+  uint32_t wphase = 0;
+  auto prefetch = [&](int64_t row) {  // this warp's slice of `row`; lanes 0..7 issue
+    if (row >= rows) return;
+    if (lane == 0) mbar_expect_tx(wbar, (uint32_t)(2 * 512 * sizeof(T)));
+    __syncwarp();
+    if (lane < 8) {
+      const T* src = (lane < 4 ? X : P) + row * (int64_t)D + 512 * sw + 128 * (lane & 3);
+      bulk_g2s(wbuf + (lane >> 2) * 4 * RS + (lane & 3) * RS, src, (uint32_t)(128 * sizeof(T)), wbar);
+    }
+  };
+  if (lane == 0) {
+    mbar_init(wbar, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();  // gbest staged, barriers initialised
+  prefetch((int64_t)blockIdx.x * RPC + slot);
+
+  double best_f = CUDART_INF;
+  int64_t best_i = INT64_MAX;
+  for (int64_t r0 = (int64_t)blockIdx.x * RPC; r0 < rows; r0 += rstride) {  // CTA-uniform
+    const int64_t r = r0 + slot;
+    const bool rv = r < rows;
+    const int64_t gi = p.row_lo + r;
+    T x[M];
+    const double pf_row = (rv && sw == 0) ? p.p_f[r] : 0.0;  // needed after barrier A
+    if (rv) {
+      T pv[M];
+      mbar_wait(wbar, wphase);
+      wphase ^= 1;
+      const T* xs = reinterpret_cast<const T*>(wbuf + s * RS);
+      const T* ps = reinterpret_cast<const T*>(wbuf + 4 * RS + s * RS);
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        x[m] = xs[k + 8 * m];
+        pv[m] = ps[k + 8 * m];
+      }
+      __syncwarp();
+      fence_proxy_async();
+      prefetch(r + rstride);
+
+      // ---- positions (core.py:138-173; see k_chain)
+      T* xr = X + r * (int64_t)D;
+      if constexpr (RNG == 0) {
+        const uint64_t xb = xs30(fold64(rootb, (uint64_t)gi)), xf = xs30(fold64(rootf, (uint64_t)gi));
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          const int j = jb + 8 * m;
+          const uint64_t gx = xs30(g0 + GAMMA * (uint64_t)(8 * m));
+          const uint64_t kb = mix64_tail(xb ^ gx) >> 11;
+          const double fresh =
+              __dadd_rn(p.var_min, __dmul_rn(p.span53, (double)(mix64_tail(xf ^ gx) >> 11)));
+          T v = x[m];
+          v = kb >= p.Kw ? pv[m] : v;
+          v = kb >= p.Kp ? gb[j] : v;
+          v = kb >= p.Kg ? (T)fresh : v;
+          x[m] = v;
+          stg_stream<T, 1>(xr + j, VecT<T, 1>{{v}});
+        }
+      } else {
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          const int j = jb + 8 * m;
+          VecT<T, 1> xv{{x[m]}}, pb{{pv[m]}}, gv{{gb[j]}};
+          x[m] = search_chunk<T, 1, 1>(p, xv, pb, gv, 0, 0, j, (uint64_t)gi, t).v[0];
+          stg_stream<T, 1>(xr + j, VecT<T, 1>{{x[m]}});
+        }
+      }
+
+      // ---- leaf chains (lane k: r[k] of leaf 4sw+s) and the 8-lane combine
+      T a1 = (T)0, a2 = (T)0;
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        const T v1 = chain_term1<T, FN>(x[m], (T)0, jb + 8 * m);
+        a1 = m == 0 ? v1 : N::add(a1, v1);
+        if constexpr (two_sums(FN)) {
+          const T v2 = Trig<T>::cos2pi(x[m]);
+          a2 = m == 0 ? v2 : N::add(a2, v2);
+        }
+      }
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) {
+        a1 = N::add(a1, __shfl_xor_sync(0xffffffffu, a1, o));
+        if constexpr (two_sums(FN)) a2 = N::add(a2, __shfl_xor_sync(0xffffffffu, a2, o));
+      }
+      if (k == 0) {
+        leafv[(slot * 2) * NL + 4 * sw + s] = (double)a1;
+        leafv[(slot * 2 + 1) * NL + 4 * sw + s] = (double)a2;
+      }
+    }
+    __syncthreads();  // (A) all leaves of the CTA's rows are in smem
+
+    if (rv && sw == 0) {  // one warp per row: balanced tree over the 4W leaves
+      const T x0 = __shfl_sync(0xffffffffu, x[0], 0);
+      T s1 = (T)0, s2 = (T)0;
+      if (lane < NL) {
+        s1 = (T)leafv[(slot * 2) * NL + lane];
+        s2 = (T)leafv[(slot * 2 + 1) * NL + lane];
+      }
+#pragma unroll
+      for (int o = 1; o < NL; o <<= 1) {
+        s1 = N::add(s1, __shfl_xor_sync(0xffffffffu, s1, o));
+        if constexpr (two_sums(FN)) s2 = N::add(s2, __shfl_xor_sync(0xffffffffu, s2, o));
+      }
+      if (lane == 0) {
+        const double f = finish<T, FN>(s1, s2, (T)1, D, &x0, p.probe_level);
+        if (!isfinite(f) && p.bad)
+          atomicMin(p.bad, ((unsigned long long)(t + 1) << 40) | (unsigned long long)gi);
+        if (p.sol_f && ((mode & M_SOLF) || !isfinite(f))) p.sol_f[r] = f;
+        const bool imp = f <= pf_row;  // parallel.py:109, ties refresh
+        const double pf = imp ? f : pf_row;
+        if (imp) p.p_f[r] = f;
+        flag[slot] = imp;
+        if (lex_less(pf, gi, best_f, best_i)) { best_f = pf; best_i = gi; }
+      }
+    }
+    __syncthreads();  // (B) pbest decisions visible; leafv free for the next round
+    if (rv && flag[slot]) {
+      T* pr = P + r * (int64_t)D;
+#pragma unroll
+      for (int m = 0; m < M; ++m) stg_stream<T, 1>(pr + jb + 8 * m, VecT<T, 1>{{x[m]}});
+    }
+  }
+
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double of = __shfl_xor_sync(0xffffffffu, best_f, o);
+    const int64_t oi = __shfl_xor_sync(0xffffffffu, best_i, o);
+    if (lex_less(of, oi, best_f, best_i)) { best_f = of; best_i = oi; }
+  }
+  if (lane == 0) { red_f[warp] = best_f; red_i[warp] = best_i; }
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < NW; ++w)
+      if (lex_less(red_f[w], red_i[w], best_f, best_i)) { best_f = red_f[w]; best_i = red_i[w]; }
+    p.slot_f[blockIdx.x] = best_f;
+    p.slot_i[blockIdx.x] = best_i;
+  }
+}
+
 }  // namespace psso

@@ -13,6 +13,16 @@ const void* chain_kernel_f64_philox(int fn, int m, bool init, bool full);
 const void* chain_kernel_f32_ref(int fn, int m, bool init, bool full);
 const void* chain_kernel_f32_philox(int fn, int m, bool init, bool full);
 
+const void* rows_kernel_f64_ref(int fn, int w);
+const void* rows_kernel_f64_philox(int fn, int w);
+const void* rows_kernel_f32_ref(int fn, int w);
+const void* rows_kernel_f32_philox(int fn, int w);
+
+inline const void* rows_kernel(int dtype, int rng, int fn, int w) {
+  if (dtype == 0) return rng == 0 ? rows_kernel_f64_ref(fn, w) : rows_kernel_f64_philox(fn, w);
+  return rng == 0 ? rows_kernel_f32_ref(fn, w) : rows_kernel_f32_philox(fn, w);
+}
+
 inline const void* chain_kernel(int dtype, int rng, int fn, int m, bool init, bool full) {
   if (dtype == 0)
     return rng == 0 ? chain_kernel_f64_ref(fn, m, init, full) : chain_kernel_f64_philox(fn, m, init, full);

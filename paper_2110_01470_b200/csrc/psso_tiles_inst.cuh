@@ -44,4 +44,20 @@ const void* PSSO_NAME(chain_kernel)(int fn, int m, bool init, bool full) {
   }
 }
 
+#define PSSO_ROWS(FN)                                                 \
+  case FN:                                                            \
+    if (w == 1) return (const void*)k_rows<PSSO_T, FN, PSSO_RNG, 1>;  \
+    if (w == 2) return (const void*)k_rows<PSSO_T, FN, PSSO_RNG, 2>;  \
+    if (w == 4) return (const void*)k_rows<PSSO_T, FN, PSSO_RNG, 4>;  \
+    if (w == 8) return (const void*)k_rows<PSSO_T, FN, PSSO_RNG, 8>;  \
+    return nullptr;
+
+const void* PSSO_NAME(rows_kernel)(int fn, int w) {
+  switch (fn) {
+    PSSO_ROWS(0) PSSO_ROWS(1) PSSO_ROWS(2) PSSO_ROWS(5) PSSO_ROWS(6) PSSO_ROWS(9)
+    default:
+      return nullptr;
+  }
+}
+
 }  // namespace psso

@@ -376,6 +376,12 @@ def _oracle_run(fid, p, seed, niter, threads=None):
     ("f4", 1 << 17, 64, 4),    # C4 row shape
     ("f6", 1024, 4096, 3),     # C5 row shape (multi-leaf rows)
     ("f7", 4096, 100, 5),      # C2 shape (sequential product, aux table)
+    # chain kernel, compile-time row shapes (D = 8M) with ragged last groups
+    ("f5", 4099, 32, 6), ("f4", 4099, 32, 6), ("f1", 1003, 64, 6), ("f9", 515, 128, 5),
+    ("f2", 1001, 128, 5),
+    # row-split kernel k_rows: D = 512 W, W = 1, 2, 4, 8, rows not a multiple of 8 / W
+    ("f6", 1021, 512, 4), ("f2", 257, 1024, 3), ("f5", 130, 2048, 3), ("f9", 77, 4096, 3),
+    ("f1", 333, 512, 4),
 ])
 def test_large_shapes_against_oracle(fid, nsol, nvar, niter):
     fn = psso.make_function(fid, nvar)
