@@ -577,13 +577,16 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
         const int es = cfg->dtype == PSSO_F64 ? 8 : 4;
         // gbest | warp reduction + xs30(gamma*(j+1)) table | per-warp mbarriers |
         // per-warp prefetch buffers (FULL iteration kernel, psso_device.cuh)
+        // | per-warp smem rows (f3, f7, f8)
         const int nw = PSSO_CHAIN_NT / 32;
+        const bool smem_fn = cfg->fn_id == 3 || cfg->fn_id == 7 || cfg->fn_id == 8;
         c->LF.off_red = (int)align16((size_t)D * es);
         c->LF.off_bar = (int)align16((size_t)c->LF.off_red + 128 + 64 * M);
         c->LF.off_xs = (int)((c->LF.off_bar + 8 * nw + 127) & ~127);
-        c->LF.smem = full && PSSO_CHAIN_PF ? (size_t)c->LF.off_xs + (size_t)nw * 8 * (8 * M + 8) * es
-                                           : (size_t)c->LF.off_bar;
-        c->init_smem = (size_t)c->LF.off_bar;
+        c->LF.off_scr = (int)align16((size_t)c->LF.off_xs +
+                                     (full && PSSO_CHAIN_PF ? (size_t)nw * 8 * (8 * M) * es : 0));
+        c->LF.smem = (size_t)c->LF.off_scr + (smem_fn ? (size_t)nw * 4 * (8 * M) * es : 0);
+        c->init_smem = c->LF.smem;
       }
     }
   }
@@ -601,12 +604,12 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
       c->rows_w = W;
       const int es = cfg->dtype == PSSO_F64 ? 8 : 4;
       // gbest | warp reduction | leaf values [8/W][2][4W] | flags | mbarriers | prefetch buffers
-      c->LF.off_red = (int)align16((size_t)D * es);
+      c->LF.off_red = (int)align16((size_t)(D + D / 16) * es);  // gbest padded per leaf
       c->LF.off_leaf = c->LF.off_red + 128;
       c->LF.off_flag = c->LF.off_leaf + 512;
       c->LF.off_bar = (int)align16((size_t)c->LF.off_flag + 32);
       c->LF.off_xs = (int)((c->LF.off_bar + 64 + 127) & ~127);
-      c->LF.smem = (size_t)c->LF.off_xs + 8 * 8 * (size_t)(128 + 8) * es;
+      c->LF.smem = (size_t)c->LF.off_xs + 8 * 8 * (size_t)128 * es;
     }
   }
   if (!c->tile_fn || !c->fused_fn) {
@@ -617,7 +620,8 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
   if ((e = cudaGetDevice(&c->device)) != cudaSuccess ||
       (e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device)) != cudaSuccess ||
       (e = cudaFuncSetAttribute(c->tile_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->L.smem)) != cudaSuccess ||
-      (e = cudaFuncSetAttribute(c->fused_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->LF.smem)) != cudaSuccess) {
+      (e = cudaFuncSetAttribute(c->fused_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->LF.smem)) != cudaSuccess ||
+      (c->chain && (e = cudaFuncSetAttribute(c->init_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->init_smem)) != cudaSuccess)) {
     delete c;
     return cuda_fail(nullptr, e, "psso_create");
   }

@@ -924,8 +924,8 @@ __global__ void __launch_bounds__(NT, 2) k_fused(const __grid_constant__ TilePar
 }
 
 // --------------------------------------------------------------- k_chain ----
-// Hot path for rows whose objective is one pairwise leaf (n <= 128 terms) of
-// position-local terms (f1, f2, f4, f5, f6, f9 and the probe): C1-C4.
+// Hot path for rows whose objective is one pairwise leaf (n <= 128 terms):
+// C1-C4 and every objective at D <= 128.
 //
 // "Chain mapping": 8 consecutive lanes own one particle; lane k holds the
 // positions j = k + 8m (m < M) in registers -- exactly the elements numpy's
@@ -936,14 +936,15 @@ __global__ void __launch_bounds__(NT, 2) k_fused(const __grid_constant__ TilePar
 //   ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7))) -> tail terms summed in order
 //   -> fitness (identical on the 8 lanes) -> pbest <= test -> improved rows
 //   written to P from registers.
-// A warp runs 4 particles at a time, persistent over the swarm; no shared
-// memory beyond the CTA's gbest copy, no __syncthreads in the loop.
-// f4's neighbour x[j+1] comes from lane k+1 (same m) or, for k = 7, from
-// lane 0 at m+1, with a single shuffle (lane 0 provides x[m+1]).
+// A warp runs 4 particles at a time, persistent over the swarm; no
+// __syncthreads in the loop.  f4's neighbour x[j+1] comes from lane k+1
+// (same m) or, for k = 7, from lane 0 at m+1, with a single shuffle.  The
+// objectives with sequential or grouped terms go through a per-warp smem row:
+// f3 (cumsum, benchmarks.py:117-119) and f7's product (:143-148) are formed
+// left to right by the segment's lane 0 exactly like numpy; f8's grouped
+// terms (:151-162) are read from the row by the chain lanes.
 template <int FN>
-__host__ __device__ constexpr bool chain_fn() {
-  return FN == 0 || FN == 1 || FN == 2 || FN == 4 || FN == 5 || FN == 6 || FN == 9;
-}
+__host__ __device__ constexpr bool chain_smem_fn() { return FN == 3 || FN == 7 || FN == 8; }
 
 template <typename T, int FN>
 __device__ __forceinline__ T chain_term1(T x, T nb, int e) {
@@ -962,7 +963,7 @@ __device__ __forceinline__ T chain_term1(T x, T nb, int e) {
     else return __fmaf_rn(p, c, N::mul(x, x));
   } else if constexpr (FN == 9) {
     return N::mul(x, Trig<T>::sin_(N::sqrt_(fabs(x))));
-  } else {  // 0, 1, 6
+  } else {  // 0, 1, 6, 7 (the x*x sum)
     return N::mul(x, x);
   }
 }
@@ -977,58 +978,264 @@ __device__ __forceinline__ T chain_term1(T x, T nb, int e) {
 #define PSSO_CHAIN_PF 1  // FULL iteration kernel: TMA prefetch of the next group
 #endif
 
-// Shared-memory row stride of the chain kernel's per-warp prefetch buffer:
-// rows padded by 8 elements so the four 8-lane segments of a warp read
-// disjoint banks (fp64: two wavefronts per LDS.64, fp32: one per LDS.32).
+// Shared-memory row stride of the chain kernels' per-warp prefetch buffer:
+// dense rows, so each array of a group arrives with ONE bulk copy (the four
+// 8-lane segments then share banks: 2x the minimum LDS wavefronts, cheaper
+// than the issue cost of one copy per padded row).
 template <typename T, int M>
-__host__ __device__ constexpr int chain_row_stride() { return (8 * M + 8) * (int)sizeof(T); }
+__host__ __device__ constexpr int chain_row_stride() { return 8 * M * (int)sizeof(T); }
 
+// Per-launch constants of the chain step.
+struct ChainEnv {
+  uint64_t rootb, rootf;  // keyed roots of the BRANCH/FRESH (or INIT) streams at t
+  int64_t t;
+  int D, n, mlen, tail;   // row length, terms, full chains, tail terms
+};
+
+// One group step of the chain mapping: the segment's row r (rv: r exists;
+// x holds the loaded positions, pv the pbests unless INIT).  Positions, X
+// store, fitness in numpy order, pbest/p_f/sol_f bookkeeping and the
+// lexicographic candidate.  The whole warp must call it (shuffles).
+template <typename T, int FN, int RNG, int M, bool INIT, bool FULL>
+__device__ __forceinline__ void chain_step(const TileParams& p, const ChainEnv& ev, const T* gb,
+                                           const uint64_t* xg, T* scr, int64_t r, bool rv,
+                                           T (&x)[M], const T (&pv)[M], double pf_row,
+                                           double& best_f, int64_t& best_i) {
+  using N = Num<T>;
+  const int lane = threadIdx.x & 31, k = lane & 7, seg = lane & ~7;
+  const int D = ev.D;
+  const int64_t gi = p.row_lo + r;
+  T* __restrict__ xr = reinterpret_cast<T*>(p.X) + r * (int64_t)D;
+  T* __restrict__ pr = reinterpret_cast<T*>(p.P) + r * (int64_t)D;
+  const int mode = INIT ? (M_INIT | M_EVAL | M_CAND | M_SOLF)
+                        : (M_SEARCH | M_EVAL | M_PBEST | M_CAND | (p.mode & M_SOLF));
+
+  // ---- positions
+  if constexpr (INIT) {
+    uint64_t hb = 0;
+    if constexpr (RNG == 0) hb = fold64(ev.rootb, (uint64_t)gi);
+    uint64_t g = GAMMA * (uint64_t)(k + 1);
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const int j = k + 8 * m;
+      if (rv && (FULL || j < D)) {
+        uint64_t h;
+        if constexpr (RNG == 0) {
+          h = mix64(hb ^ g);
+        } else {
+          Philox4 w = philox4x32_10((uint32_t)(j >> 1), (uint32_t)gi, (uint32_t)(gi >> 32),
+                                    0xFFFFFFFFu, (uint32_t)p.seed, (uint32_t)(p.seed >> 32));
+          const int s2 = (j & 1) * 2;
+          h = ((uint64_t)w.w[s2] << 32) | w.w[s2 + 1];
+        }
+        const T v = (T)__dadd_rn(p.var_min, __dmul_rn(p.span, unit53(h)));
+        stg_stream<T, 1>(pr + j, VecT<T, 1>{{v}});
+        x[m] = v;
+        stg_stream<T, 1>(xr + j, VecT<T, 1>{{v}});
+      } else {
+        x[m] = (T)0;
+      }
+      g += GAMMA * 8ull;
+    }
+  } else {
+    // core.py:138-173, branch-free (see search_chunk).  Reference RNG:
+    // mix64(h ^ g) = mix64_tail(xs30(h) ^ xs30(g)) since the first
+    // xorshift is linear over xor; xs30(g_j) comes from the CTA's table.
+    uint64_t xb = 0, xf = 0;
+    if constexpr (RNG == 0) {
+      xb = xs30(fold64(ev.rootb, (uint64_t)gi));
+      xf = xs30(fold64(ev.rootf, (uint64_t)gi));
+    }
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const int j = k + 8 * m;
+      T v;
+      if constexpr (RNG == 0) {
+        const uint64_t gx = xg[j];
+        const uint64_t kb = mix64_tail(xb ^ gx) >> 11;
+        const double fresh =
+            __dadd_rn(p.var_min, __dmul_rn(p.span53, (double)(mix64_tail(xf ^ gx) >> 11)));
+        v = x[m];
+        v = kb >= p.Kw ? pv[m] : v;
+        v = kb >= p.Kp ? gb[j] : v;
+        v = kb >= p.Kg ? (T)fresh : v;
+      } else {
+        VecT<T, 1> xv{{x[m]}}, pb{{pv[m]}}, gv{{gb[j]}};
+        v = search_chunk<T, 1, 1>(p, xv, pb, gv, 0, 0, j, (uint64_t)gi, ev.t).v[0];
+      }
+      x[m] = v;
+      if (rv && (FULL || j < D)) stg_stream<T, 1>(xr + j, VecT<T, 1>{{v}});
+    }
+  }
+
+  // ---- sequential / grouped objectives: the segment's row in smem
+  T* row = scr + (lane >> 3) * (8 * M);
+  T prod = (T)1;
+  if constexpr (chain_smem_fn<FN>()) {
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const int j = k + 8 * m;
+      if (FULL || j < D) {
+        if constexpr (FN == 7) row[j] = N::cos_(N::mul(x[m], (T)p.aux[j]));  // factors
+        else row[j] = x[m];
+      }
+    }
+    __syncwarp();
+    if constexpr (FN == 3) {  // c = cumsum(x) left to right, terms c*c in place
+      if (k == 0) {
+        T c = row[0];
+        row[0] = N::mul(c, c);
+        for (int j = 1; j < D; ++j) {
+          c = N::add(c, row[j]);
+          row[j] = N::mul(c, c);
+        }
+      }
+      __syncwarp();
+    } else if constexpr (FN == 7) {  // prod(cos(x * inv)) left to right
+      if (k == 0)
+        for (int j = 0; j < D; ++j) prod = N::mul(prod, row[j]);
+      prod = __shfl_sync(0xffffffffu, prod, seg);
+    }
+  }
+
+  // ---- fitness: lane k accumulates terms k, k+8, ... in order
+  T a1 = (T)0, a2 = (T)0, t1 = (T)0, t2 = (T)0;
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const int e = k + 8 * m;
+    T nb = (T)0;
+    if constexpr (FN == 4) {
+      const T nxt = (m + 1 < M) ? x[m + 1 < M ? m + 1 : m] : (T)0;
+      const T prov = (k == 0) ? nxt : x[m];
+      nb = __shfl_sync(0xffffffffu, prov, k < 7 ? lane + 1 : lane - 7);
+    }
+    if (m < ev.mlen || (m == ev.mlen && k < ev.tail)) {
+      T v1;
+      if constexpr (FN == 3) v1 = row[e];
+      else if constexpr (FN == 8) v1 = heavy_term<T, 8>(row, e);
+      else v1 = chain_term1<T, FN>(x[m], nb, e);
+      T v2 = (T)0;
+      if constexpr (two_sums(FN)) v2 = Trig<T>::cos2pi(x[m]);
+      if (m < ev.mlen) {
+        a1 = (m == 0) ? v1 : N::add(a1, v1);
+        if constexpr (two_sums(FN)) a2 = (m == 0) ? v2 : N::add(a2, v2);
+      } else {
+        t1 = v1;
+        t2 = v2;
+      }
+    }
+  }
+  if constexpr (chain_smem_fn<FN>()) __syncwarp();  // row reads done before the next group
+  a1 = N::add(a1, __shfl_xor_sync(0xffffffffu, a1, 1));
+  a1 = N::add(a1, __shfl_xor_sync(0xffffffffu, a1, 2));
+  a1 = N::add(a1, __shfl_xor_sync(0xffffffffu, a1, 4));
+  if constexpr (two_sums(FN)) {
+    a2 = N::add(a2, __shfl_xor_sync(0xffffffffu, a2, 1));
+    a2 = N::add(a2, __shfl_xor_sync(0xffffffffu, a2, 2));
+    a2 = N::add(a2, __shfl_xor_sync(0xffffffffu, a2, 4));
+  }
+  T s1 = ev.mlen > 0 ? a1 : (T)0;
+  T s2 = ev.mlen > 0 ? a2 : (T)0;
+  for (int q = 0; q < ev.tail; ++q) {  // numpy adds the tail left to right
+    s1 = N::add(s1, __shfl_sync(0xffffffffu, t1, seg + q));
+    if constexpr (two_sums(FN)) s2 = N::add(s2, __shfl_sync(0xffffffffu, t2, seg + q));
+  }
+  const T x0 = __shfl_sync(0xffffffffu, x[0], seg);
+  const double f = finish<T, FN>(s1, s2, prod, D, &x0, p.probe_level);
+
+  // ---- bookkeeping (identical on the 8 lanes; lane k == 0 writes)
+  if (rv) {
+    if (k == 0) {
+      if (!isfinite(f) && p.bad)
+        atomicMin(p.bad, ((unsigned long long)(ev.t + 1) << 40) | (unsigned long long)gi);
+      if (p.sol_f && ((mode & M_SOLF) || !isfinite(f))) p.sol_f[r] = f;
+    }
+    double pf = f;
+    if (INIT) {
+      if (k == 0) p.p_f[r] = f;
+    } else {
+      const bool imp = f <= pf_row;  // parallel.py:109, ties refresh
+      pf = imp ? f : pf_row;
+      if (imp) {
+        if (k == 0) p.p_f[r] = f;
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          const int j = k + 8 * m;
+          if (FULL || j < D) stg_stream<T, 1>(pr + j, VecT<T, 1>{{x[m]}});
+        }
+      }
+    }
+    if (k == 0 && lex_less(pf, gi, best_f, best_i)) { best_f = pf; best_i = gi; }
+  }
+}
+
+// Deterministic CTA argmin of the per-thread candidates -> slot (no atomics).
+template <int NW>
+__device__ __forceinline__ void cta_candidate(double best_f, int64_t best_i, double* red_f,
+                                              int64_t* red_i, double* slot_f, int64_t* slot_i) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double of = __shfl_xor_sync(0xffffffffu, best_f, o);
+    const int64_t oi = __shfl_xor_sync(0xffffffffu, best_i, o);
+    if (lex_less(of, oi, best_f, best_i)) { best_f = of; best_i = oi; }
+  }
+  if (lane == 0) { red_f[warp] = best_f; red_i[warp] = best_i; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < NW; ++w)
+      if (lex_less(red_f[w], red_i[w], best_f, best_i)) { best_f = red_f[w]; best_i = red_i[w]; }
+    *slot_f = best_f;
+    *slot_i = best_i;
+  }
+}
+
+// Shared memory of the chain kernels (offsets in TileParams, host: chain_layout):
+//   off 0      gbest (D of T)
+//   off_red    warp reduction (16 * NW bytes) + xs30(gamma*(j+1)) table (8 * 8M)
+//   off_bar    per-warp mbarriers
+//   off_xs     per-warp prefetch buffers (FULL iteration kernel): [X 4 rows][P 4 rows]
+//   off_scr    per-warp smem rows [4][8M] (f3, f7, f8)
 template <typename T, int FN, int RNG, int M, bool INIT, bool FULL>
 __global__ void __launch_bounds__(PSSO_CHAIN_NT, PSSO_CHAIN_MINB)
     k_chain(const __grid_constant__ TileParams p) {
-  using N = Num<T>;
   constexpr int NTC = PSSO_CHAIN_NT;
   constexpr int NW = NTC / 32;
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   T* gb = reinterpret_cast<T*>(smem);
   double* red_f = reinterpret_cast<double*>(smem + p.off_red);
   int64_t* red_i = reinterpret_cast<int64_t*>(smem + p.off_red + 8 * NW);
+  uint64_t* xg = reinterpret_cast<uint64_t*>(smem + p.off_red + 16 * NW);  // [8M]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = lane & 7;
-  const int seg = lane & ~7;  // first lane of this particle's 8-lane segment
-  const int D = p.D;
-  const int mode = INIT ? (M_INIT | M_EVAL | M_CAND | M_SOLF)
-                        : (M_SEARCH | M_EVAL | M_PBEST | M_CAND | (p.mode & M_SOLF));
+  T* scr = reinterpret_cast<T*>(smem + p.off_scr) + warp * 4 * (8 * M);
   if (!INIT && p.bad && *(volatile unsigned long long*)p.bad != ~0ull) return;
-  const int64_t t = p.t_dev ? *p.t_dev : p.t_arg;
-  T* __restrict__ X = reinterpret_cast<T*>(p.X);
-  T* __restrict__ P = reinterpret_cast<T*>(p.P);
 
-  uint64_t rootb = 0, rootf = 0;
+  ChainEnv ev;
+  ev.t = p.t_dev ? *p.t_dev : p.t_arg;
+  ev.D = p.D;
+  // FULL: D == 8*M, so the chain lengths and the tail are compile-time
+  // (f4 has D-1 terms: M-1 full chains and a 7-term tail)
+  ev.n = FULL ? (FN == 4 ? 8 * M - 1 : FN == 8 ? 2 * M : 8 * M) : p.plan.n;
+  ev.mlen = ev.n >= 8 ? (ev.n >> 3) : 0;
+  ev.tail = ev.n - 8 * ev.mlen;
+  ev.rootb = ev.rootf = 0;
   if constexpr (RNG == 0) {
     if (INIT) {
-      rootb = root64(p.seed, STREAM_INIT, 0);
+      ev.rootb = root64(p.seed, STREAM_INIT, 0);
     } else {
-      rootb = root64(p.seed, STREAM_BRANCH, (uint64_t)t);
-      rootf = root64(p.seed, STREAM_FRESH, (uint64_t)t);
+      ev.rootb = root64(p.seed, STREAM_BRANCH, (uint64_t)ev.t);
+      ev.rootf = root64(p.seed, STREAM_FRESH, (uint64_t)ev.t);
     }
   }
-  uint64_t* xg = reinterpret_cast<uint64_t*>(smem + p.off_red + 16 * NW);  // [M][8]
   if (!INIT) {
     const T* g = reinterpret_cast<const T*>(p.gbest);
-    for (int j = tid; j < D; j += NTC) gb[j] = g[j];
+    for (int j = tid; j < ev.D; j += NTC) gb[j] = g[j];
     for (int q = tid; q < 8 * M; q += NTC) xg[q] = xs30(GAMMA * (uint64_t)(q + 1));  // q = j
     __syncthreads();
   }
 
-  // FULL: D == 8*M, so the chain lengths and the tail are compile-time
-  // (f4 has D-1 terms: M-1 full chains and a 7-term tail)
-  const int n = FULL ? (FN == 4 ? 8 * M - 1 : 8 * M) : p.plan.n;  // terms (one leaf, <= 128)
-  const int mlen = n >= 8 ? (n >> 3) : 0;  // chain length
-  const int tail = n - 8 * mlen;           // tail terms, at m = mlen, lanes 0..tail-1
-  const uint64_t gam0 = GAMMA * (uint64_t)(k + 1);
-  const uint64_t gstep = GAMMA * 8ull;
   const int64_t rows = p.rows;
   const int64_t ngroups = (rows + 3) >> 2;
   double best_f = CUDART_INF;
@@ -1037,22 +1244,20 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, PSSO_CHAIN_MINB)
   // PF: each warp streams its next group of 4 rows (X and P) into a private
   // shared-memory buffer with TMA bulk copies while it computes the current
   // group from registers, so HBM reads overlap the hash/select/fitness work
-  // without costing registers.  Lanes 0..7 each copy one row of X or P.
+  // without costing registers.
   constexpr bool PF = FULL && !INIT && PSSO_CHAIN_PF;
   constexpr int RS = chain_row_stride<T, M>();
   uint64_t* wbar = reinterpret_cast<uint64_t*>(smem + p.off_bar) + warp;
   unsigned char* wbuf = smem + p.off_xs + (size_t)warp * (8 * RS);
   const int64_t gstride = (int64_t)gridDim.x * NW;
   uint32_t wphase = 0;
-  auto prefetch = [&](int64_t g) {  // whole warp calls; lanes 0..7 issue
+  auto prefetch = [&](int64_t g) {  // whole warp calls; one lane issues both copies
     if (g >= ngroups) return;
-    const int nr = (int)min((int64_t)4, rows - 4 * g);
-    if (lane == 0) mbar_expect_tx(wbar, (uint32_t)(2 * nr * 8 * M * sizeof(T)));
-    __syncwarp();
-    const int s = lane & 3;
-    if (lane < 8 && s < nr) {
-      const T* src = (lane < 4 ? X : P) + (4 * g + s) * (int64_t)(8 * M);
-      bulk_g2s(wbuf + (lane >> 2) * 4 * RS + s * RS, src, (uint32_t)(8 * M * sizeof(T)), wbar);
+    if (lane == 0) {
+      const uint32_t bytes = (uint32_t)(min((int64_t)4, rows - 4 * g) * 8 * M * sizeof(T));
+      mbar_expect_tx(wbar, 2 * bytes);
+      bulk_g2s(wbuf, reinterpret_cast<const T*>(p.X) + 4 * g * (int64_t)(8 * M), bytes, wbar);
+      bulk_g2s(wbuf + 4 * RS, reinterpret_cast<const T*>(p.P) + 4 * g * (int64_t)(8 * M), bytes, wbar);
     }
   };
   if constexpr (PF) {
@@ -1067,11 +1272,8 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, PSSO_CHAIN_MINB)
   for (int64_t grp = (int64_t)blockIdx.x * NW + warp; grp < ngroups; grp += gstride) {
     const int64_t r = 4 * grp + (lane >> 3);
     const bool rv = r < rows;
-    const int64_t gi = p.row_lo + r;
     // rows past the end (last group only) compute on a clamped row and store nothing
     const int64_t rl = rv ? r : rows - 1;
-    T* xr = X + r * (int64_t)D;
-    T* pr = P + r * (int64_t)D;
     double pf_row = 0.0;
     if (!INIT) pf_row = p.p_f[rl];
 
@@ -1091,13 +1293,13 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, PSSO_CHAIN_MINB)
       __syncwarp();  // the whole buffer is in registers before it is refilled
       fence_proxy_async();
       prefetch(grp + gstride);
-    } else if (!INIT) {
-      const T* xl = X + rl * (int64_t)D;
-      const T* pl = P + rl * (int64_t)D;
+    } else if constexpr (!INIT) {
+      const T* xl = reinterpret_cast<const T*>(p.X) + rl * (int64_t)ev.D;
+      const T* pl = reinterpret_cast<const T*>(p.P) + rl * (int64_t)ev.D;
 #pragma unroll
       for (int m = 0; m < M; ++m) {
         const int j = k + 8 * m;
-        if (FULL || j < D) {
+        if (FULL || j < ev.D) {
           x[m] = ldg_stream<T, 1>(xl + j).v[0];
           pv[m] = ldg_stream<T, 1>(pl + j).v[0];
         } else {
@@ -1105,144 +1307,13 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, PSSO_CHAIN_MINB)
           pv[m] = (T)0;
         }
       }
-    }
-    uint64_t hb = 0, hf = 0;
-    if constexpr (RNG == 0) {
-      hb = fold64(rootb, (uint64_t)gi);
-      if (!INIT) hf = fold64(rootf, (uint64_t)gi);
-    }
-
-    // ---- positions
-    if constexpr (INIT) {
-      uint64_t g = gam0;
-#pragma unroll
-      for (int m = 0; m < M; ++m) {
-        const int j = k + 8 * m;
-        if (rv && (FULL || j < D)) {
-          uint64_t h;
-          if constexpr (RNG == 0) {
-            h = mix64(hb ^ g);
-          } else {
-            Philox4 w = philox4x32_10((uint32_t)(j >> 1), (uint32_t)gi, (uint32_t)(gi >> 32),
-                                      0xFFFFFFFFu, (uint32_t)p.seed, (uint32_t)(p.seed >> 32));
-            const int s2 = (j & 1) * 2;
-            h = ((uint64_t)w.w[s2] << 32) | w.w[s2 + 1];
-          }
-          const T v = (T)__dadd_rn(p.var_min, __dmul_rn(p.span, unit53(h)));
-          stg_stream<T, 1>(pr + j, VecT<T, 1>{{v}});
-          x[m] = v;
-          stg_stream<T, 1>(xr + j, VecT<T, 1>{{v}});
-        }
-        g += gstep;
-      }
     } else {
-      // core.py:138-173, branch-free (see search_chunk).  Reference RNG:
-      // mix64(h ^ g) = mix64_tail(xs30(h) ^ xs30(g)) since the first
-      // xorshift is linear over xor; xs30(g_j) comes from the CTA's table.
-      const uint64_t xb = xs30(hb), xf = xs30(hf);
 #pragma unroll
-      for (int m = 0; m < M; ++m) {
-        const int j = k + 8 * m;
-        T v;
-        if constexpr (RNG == 0) {
-          const uint64_t gx = xg[m * 8 + k];
-          const uint64_t kb = mix64_tail(xb ^ gx) >> 11;
-          const double fresh =
-              __dadd_rn(p.var_min, __dmul_rn(p.span53, (double)(mix64_tail(xf ^ gx) >> 11)));
-          v = x[m];
-          v = kb >= p.Kw ? pv[m] : v;
-          v = kb >= p.Kp ? gb[j] : v;
-          v = kb >= p.Kg ? (T)fresh : v;
-        } else {
-          VecT<T, 1> xv{{x[m]}}, pb{{pv[m]}}, gv{{gb[j]}};
-          v = search_chunk<T, 1, 1>(p, xv, pb, gv, 0, 0, j, (uint64_t)gi, t).v[0];
-        }
-        x[m] = v;
-        if (rv && (FULL || j < D)) stg_stream<T, 1>(xr + j, VecT<T, 1>{{v}});
-      }
+      for (int m = 0; m < M; ++m) pv[m] = (T)0;
     }
-
-    // ---- fitness: lane k accumulates terms k, k+8, ... in order
-    T a1 = (T)0, a2 = (T)0, t1 = (T)0, t2 = (T)0;
-#pragma unroll
-    for (int m = 0; m < M; ++m) {
-      const int e = k + 8 * m;
-      T nb = (T)0;
-      if constexpr (FN == 4) {
-        const T nxt = (m + 1 < M) ? x[m + 1 < M ? m + 1 : m] : (T)0;
-        const T prov = (k == 0) ? nxt : x[m];
-        nb = __shfl_sync(0xffffffffu, prov, k < 7 ? lane + 1 : lane - 7);
-      }
-      if (m < mlen || (m == mlen && k < tail)) {
-        const T v1 = chain_term1<T, FN>(x[m], nb, e);
-        T v2 = (T)0;
-        if constexpr (two_sums(FN)) v2 = Trig<T>::cos2pi(x[m]);
-        if (m < mlen) {
-          a1 = (m == 0) ? v1 : N::add(a1, v1);
-          if constexpr (two_sums(FN)) a2 = (m == 0) ? v2 : N::add(a2, v2);
-        } else {
-          t1 = v1;
-          t2 = v2;
-        }
-      }
-    }
-    a1 = N::add(a1, __shfl_xor_sync(0xffffffffu, a1, 1));
-    a1 = N::add(a1, __shfl_xor_sync(0xffffffffu, a1, 2));
-    a1 = N::add(a1, __shfl_xor_sync(0xffffffffu, a1, 4));
-    if constexpr (two_sums(FN)) {
-      a2 = N::add(a2, __shfl_xor_sync(0xffffffffu, a2, 1));
-      a2 = N::add(a2, __shfl_xor_sync(0xffffffffu, a2, 2));
-      a2 = N::add(a2, __shfl_xor_sync(0xffffffffu, a2, 4));
-    }
-    T s1 = mlen > 0 ? a1 : (T)0;
-    T s2 = mlen > 0 ? a2 : (T)0;
-    for (int q = 0; q < tail; ++q) {  // numpy adds the tail left to right
-      s1 = N::add(s1, __shfl_sync(0xffffffffu, t1, seg + q));
-      if constexpr (two_sums(FN)) s2 = N::add(s2, __shfl_sync(0xffffffffu, t2, seg + q));
-    }
-    const T x0 = __shfl_sync(0xffffffffu, x[0], seg);
-    const double f = finish<T, FN>(s1, s2, (T)1, D, &x0, p.probe_level);
-
-    // ---- bookkeeping (identical on the 8 lanes; lane k == 0 writes)
-    if (rv) {
-      if (k == 0) {
-        if (!isfinite(f) && p.bad)
-          atomicMin(p.bad, ((unsigned long long)(t + 1) << 40) | (unsigned long long)gi);
-        if (p.sol_f && ((mode & M_SOLF) || !isfinite(f))) p.sol_f[r] = f;
-      }
-      double pf = f;
-      if (INIT) {
-        if (k == 0) p.p_f[r] = f;
-      } else {
-        const bool imp = f <= pf_row;  // parallel.py:109, ties refresh
-        pf = imp ? f : pf_row;
-        if (imp) {
-          if (k == 0) p.p_f[r] = f;
-#pragma unroll
-          for (int m = 0; m < M; ++m) {
-            const int j = k + 8 * m;
-            if (FULL || j < D) stg_stream<T, 1>(pr + j, VecT<T, 1>{{x[m]}});
-          }
-        }
-      }
-      if (k == 0 && lex_less(pf, gi, best_f, best_i)) { best_f = pf; best_i = gi; }
-    }
+    chain_step<T, FN, RNG, M, INIT, FULL>(p, ev, gb, xg, scr, r, rv, x, pv, pf_row, best_f, best_i);
   }
-
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double of = __shfl_xor_sync(0xffffffffu, best_f, o);
-    const int64_t oi = __shfl_xor_sync(0xffffffffu, best_i, o);
-    if (lex_less(of, oi, best_f, best_i)) { best_f = of; best_i = oi; }
-  }
-  if (lane == 0) { red_f[warp] = best_f; red_i[warp] = best_i; }
-  __syncthreads();
-  if (tid == 0) {
-    for (int w = 1; w < NW; ++w)
-      if (lex_less(red_f[w], red_i[w], best_f, best_i)) { best_f = red_f[w]; best_i = red_i[w]; }
-    p.slot_f[blockIdx.x] = best_f;
-    p.slot_i[blockIdx.x] = best_i;
-  }
+  cta_candidate<NW>(best_f, best_i, red_f, red_i, p.slot_f + blockIdx.x, p.slot_i + blockIdx.x);
 }
 
 // ---------------------------------------------------------------- k_rows ----
@@ -1291,11 +1362,12 @@ __global__ void __launch_bounds__(256, 2) k_rows(const __grid_constant__ TilePar
     rootb = root64(p.seed, STREAM_BRANCH, (uint64_t)t);
     rootf = root64(p.seed, STREAM_FRESH, (uint64_t)t);
   }
-  {
+  {  // gbest padded by 8 elements per leaf: the segments' reads hit disjoint banks
     const T* g = reinterpret_cast<const T*>(p.gbest);
-    for (int j = tid; j < D; j += 256) gb[j] = g[j];
+    for (int j = tid; j < D; j += 256) gb[j + ((j >> 7) << 3)] = g[j];
   }
   const int jb = 512 * sw + 128 * s + k;  // this lane's first element; j = jb + 8m
+  const T* gbl = gb + 8 * (4 * sw + s);   // gbest of this lane's leaf: gbl[j]
   const uint64_t g0 = GAMMA * (uint64_t)(jb + 1);
 
   const int64_t rows = p.rows;
@@ -1303,13 +1375,14 @@ __global__ void __launch_bounds__(256, 2) k_rows(const __grid_constant__ TilePar
   uint64_t* wbar = reinterpret_cast<uint64_t*>(smem + p.off_bar) + warp;
   unsigned char* wbuf = smem + p.off_xs + (size_t)warp * (8 * RS);
   uint32_t wphase = 0;
-  auto prefetch = [&](int64_t row) {  // this warp's slice of `row`; lanes 0..7 issue
+  auto prefetch = [&](int64_t row) {  // this warp's slice of `row`; one lane issues
     if (row >= rows) return;
-    if (lane == 0) mbar_expect_tx(wbar, (uint32_t)(2 * 512 * sizeof(T)));
-    __syncwarp();
-    if (lane < 8) {
-      const T* src = (lane < 4 ? X : P) + row * (int64_t)D + 512 * sw + 128 * (lane & 3);
-      bulk_g2s(wbuf + (lane >> 2) * 4 * RS + (lane & 3) * RS, src, (uint32_t)(128 * sizeof(T)), wbar);
+    if (lane == 0) {
+      constexpr uint32_t SB = (uint32_t)(512 * sizeof(T));  // bytes per slice
+      mbar_expect_tx(wbar, 2 * SB);
+      const int64_t off = row * (int64_t)D + 512 * sw;
+      bulk_g2s(wbuf, X + off, SB, wbar);
+      bulk_g2s(wbuf + 4 * RS, P + off, SB, wbar);
     }
   };
   if (lane == 0) {
@@ -1355,7 +1428,7 @@ __global__ void __launch_bounds__(256, 2) k_rows(const __grid_constant__ TilePar
               __dadd_rn(p.var_min, __dmul_rn(p.span53, (double)(mix64_tail(xf ^ gx) >> 11)));
           T v = x[m];
           v = kb >= p.Kw ? pv[m] : v;
-          v = kb >= p.Kp ? gb[j] : v;
+          v = kb >= p.Kp ? gbl[j] : v;
           v = kb >= p.Kg ? (T)fresh : v;
           x[m] = v;
           stg_stream<T, 1>(xr + j, VecT<T, 1>{{v}});
@@ -1364,7 +1437,7 @@ __global__ void __launch_bounds__(256, 2) k_rows(const __grid_constant__ TilePar
 #pragma unroll
         for (int m = 0; m < M; ++m) {
           const int j = jb + 8 * m;
-          VecT<T, 1> xv{{x[m]}}, pb{{pv[m]}}, gv{{gb[j]}};
+          VecT<T, 1> xv{{x[m]}}, pb{{pv[m]}}, gv{{gbl[j]}};
           x[m] = search_chunk<T, 1, 1>(p, xv, pb, gv, 0, 0, j, (uint64_t)gi, t).v[0];
           stg_stream<T, 1>(xr + j, VecT<T, 1>{{x[m]}});
         }

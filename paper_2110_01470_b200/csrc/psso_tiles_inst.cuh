@@ -37,8 +37,8 @@ const void* PSSO_NAME(tile_kernel)(int fn, int vec, bool fused) {
 
 const void* PSSO_NAME(chain_kernel)(int fn, int m, bool init, bool full) {
   switch (fn) {
-    PSSO_CHAIN(0) PSSO_CHAIN(1) PSSO_CHAIN(2) PSSO_CHAIN(4) PSSO_CHAIN(5) PSSO_CHAIN(6)
-    PSSO_CHAIN(9)
+    PSSO_CHAIN(0) PSSO_CHAIN(1) PSSO_CHAIN(2) PSSO_CHAIN(3) PSSO_CHAIN(4) PSSO_CHAIN(5)
+    PSSO_CHAIN(6) PSSO_CHAIN(7) PSSO_CHAIN(8) PSSO_CHAIN(9)
     default:
       return nullptr;
   }
