@@ -15,6 +15,7 @@
 #include "psso.h"
 #include "psso_device.cuh"
 #include "psso_registry.h"
+#include "psso_swarm.cuh"
 
 using namespace psso;
 
@@ -24,6 +25,9 @@ thread_local std::string g_err;
 
 constexpr int GB_THREADS = 256;
 constexpr int GRAPH_CHUNK = 16;  // iterations per captured graph
+#ifndef PSSO_SWARM_MAX_ELEMS
+#define PSSO_SWARM_MAX_ELEMS (1 << 22)  // N*D up to which psso_run uses the whole-run kernel
+#endif
 
 struct Layout {
   int V, R, G, S, NL;
@@ -358,6 +362,17 @@ struct psso_ctx {
   bool profiling;
   std::vector<cudaEvent_t> ev;
   size_t ev_used;
+  int64_t prof_iters;    // iterations covered by the timed launches
+  // whole-run kernel for small swarms (psso_swarm.cuh); null: streaming path
+  const void* swarm_fn;
+  int swarm_G;
+  size_t swarm_smem;
+  int swarm_off_bar, swarm_off_scr;
+  unsigned int* sw_bar;
+  double* sw_slot_f;
+  int64_t* sw_slot_i;
+  void* sw_slot_row;
+  uint64_t* sw_seed;
   std::string err;
 };
 
@@ -507,6 +522,7 @@ int launch_fused(psso_ctx* c, int64_t t, int64_t* t_dev) {
   if (timed) {
     CK(c, cudaEventRecord(c->ev[c->ev_used + 1], c->stream));
     c->ev_used += 2;
+    c->prof_iters += 1;
   }
   return PSSO_OK;
 }
@@ -653,6 +669,36 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
     const int rpc = 8 / c->rows_w;
     c->fused_grid = (int)std::min<int64_t>((rows + rpc - 1) / rpc, (int64_t)per_sm_fused * c->num_sms);
   }
+  c->swarm_fn = nullptr;
+  c->swarm_G = 0;
+  if (c->chain && cfg->row_lo == 0 && cfg->row_hi == cfg->nsol &&
+      rows * cfg->nvar <= PSSO_SWARM_MAX_ELEMS) {  // small swarm: the whole run in one launch
+    const char* off = std::getenv("PSSO_NO_SWARM");
+    const int64_t D = cfg->nvar;
+    const int M = D <= 32 ? 4 : D <= 64 ? 8 : 16;
+    const void* f = (off && *off && *off != '0') ? nullptr : swarm_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, M);
+    if (f) {
+      const int es = cfg->dtype == PSSO_F64 ? 8 : 4;
+      const bool smem_fn = cfg->fn_id == 3 || cfg->fn_id == 7 || cfg->fn_id == 8;
+      // gbest | reduction + xs30 table (as k_chain) | winner record | smem rows
+      c->swarm_off_bar = (int)align16((size_t)c->LF.off_red + 128 + 64 * M);
+      c->swarm_off_scr = (int)align16((size_t)c->swarm_off_bar + 32);
+      c->swarm_smem = (size_t)c->swarm_off_scr + (smem_fn ? (size_t)(NT / 32) * 4 * (8 * M) * es : 0);
+      int per_sm_sw = 0;
+      if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->swarm_smem)) != cudaSuccess ||
+          (e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_sw, f, NT, c->swarm_smem)) != cudaSuccess) {
+        delete c;
+        return cuda_fail(nullptr, e, "psso_create swarm kernel");
+      }
+      const int64_t groups = (rows + 3) / 4;
+      const int64_t want = (groups + (NT / 32) - 1) / (NT / 32);  // one row group per warp
+      const int64_t cap = (int64_t)per_sm_sw * c->num_sms;
+      if (per_sm_sw >= 1) {
+        c->swarm_fn = f;
+        c->swarm_G = (int)std::max<int64_t>(1, std::min<int64_t>(want, cap));
+      }
+    }
+  }
   c->argmin_grid = (int)std::min<int64_t>((rows + 255) / 256, 4 * c->num_sms);
   c->nslots = std::max(std::max(std::max(c->grid, c->fused_grid), c->init_grid), c->argmin_grid);
   c->Kw = k53(cfg->cw); c->Kp = k53(cfg->cp); c->Kg = k53(cfg->cg);
@@ -665,6 +711,20 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
       (e = cudaMemset(c->bad, 0xff, sizeof(unsigned long long))) != cudaSuccess) {
     psso_destroy(c);
     return cuda_fail(nullptr, e, "psso_create alloc");
+  }
+  if (c->swarm_fn) {
+    const size_t es = cfg->dtype == PSSO_F64 ? 8 : 4;
+    const size_t G = (size_t)c->swarm_G;
+    const uint64_t seed = cfg->seed;
+    if ((e = cudaMalloc(&c->sw_bar, sizeof(unsigned int))) != cudaSuccess ||
+        (e = cudaMalloc(&c->sw_slot_f, 2 * G * sizeof(double))) != cudaSuccess ||
+        (e = cudaMalloc(&c->sw_slot_i, 2 * G * sizeof(int64_t))) != cudaSuccess ||
+        (e = cudaMalloc(&c->sw_slot_row, 2 * G * (size_t)cfg->nvar * es)) != cudaSuccess ||
+        (e = cudaMalloc(&c->sw_seed, sizeof(uint64_t))) != cudaSuccess ||
+        (e = cudaMemcpy(c->sw_seed, &seed, sizeof seed, cudaMemcpyHostToDevice)) != cudaSuccess) {
+      psso_destroy(c);
+      return cuda_fail(nullptr, e, "psso_create swarm buffers");
+    }
   }
   if (cfg->fn_id == 7) {
     if ((e = cudaMalloc(&c->aux, sizeof(double) * cfg->nvar)) != cudaSuccess) {
@@ -690,6 +750,11 @@ void psso_destroy(psso_ctx* c) {
   cudaFree(c->bad);
   cudaFree(c->t_dev);
   cudaFree(c->aux);
+  cudaFree(c->sw_bar);
+  cudaFree(c->sw_slot_f);
+  cudaFree(c->sw_slot_i);
+  cudaFree(c->sw_slot_row);
+  cudaFree(c->sw_seed);
   delete c;
 }
 
@@ -734,9 +799,60 @@ int psso_step(psso_ctx* c, int64_t t) {
   return fused_step(c, t, nullptr);
 }
 
+// the whole loop as one k_swarm launch (small swarms)
+static int swarm_run(psso_ctx* c, int64_t t0, int64_t niter) {
+  TileParams p = tile_params(c, fused_mode(c), t0, nullptr, true);
+  p.off_bar = c->swarm_off_bar;
+  p.off_scr = c->swarm_off_scr;
+  SwarmParams sp;
+  std::memset(&sp, 0, sizeof sp);
+  sp.t0 = t0;
+  sp.niter = niter;
+  sp.rows = c->cfg.row_hi - c->cfg.row_lo;
+  sp.G = c->swarm_G;
+  sp.do_init = 0;
+  sp.bar = c->sw_bar;
+  sp.slot_f = c->sw_slot_f;
+  sp.slot_i = c->sw_slot_i;
+  sp.slot_row = c->sw_slot_row;
+  sp.traj = c->buf.traj;
+  sp.traj_stride = 0;
+  sp.g_f = c->buf.g_f;
+  sp.gbest = c->buf.gbest;
+  sp.seeds = c->sw_seed;
+  sp.sol_f = c->buf.sol_f;
+  sp.bad = c->bad;
+  CK(c, cudaMemsetAsync(c->sw_bar, 0, sizeof(unsigned int), c->stream));
+  const bool timed = c->profiling;
+  if (timed) {
+    if (c->ev_used + 2 > c->ev.size()) {
+      for (int k = 0; k < 8; ++k) {
+        cudaEvent_t e;
+        CK(c, cudaEventCreate(&e));
+        c->ev.push_back(e);
+      }
+    }
+    CK(c, cudaEventRecord(c->ev[c->ev_used], c->stream));
+  }
+  void* args[] = {(void*)&p, (void*)&sp};
+  if (c->swarm_G > 1)  // co-residency of the swarm's CTAs is required by its barrier
+    CK(c, cudaLaunchCooperativeKernel(c->swarm_fn, dim3(c->swarm_G, 1), dim3(NT), args, c->swarm_smem, c->stream));
+  else
+    CK(c, cudaLaunchKernel(c->swarm_fn, dim3(1, 1), dim3(NT), args, c->swarm_smem, c->stream));
+  c->launches++;
+  if (timed) {
+    CK(c, cudaEventRecord(c->ev[c->ev_used + 1], c->stream));
+    c->ev_used += 2;
+    c->prof_iters += niter;
+  }
+  return PSSO_OK;
+}
+
 int psso_run(psso_ctx* c, int64_t t0, int64_t niter) {
   if (int rc = need_bound(c)) return rc;
   if (t0 < 0 || niter < 0) return fail(c, PSSO_E_INVALID, "t0 and niter must be >= 0");
+  if (niter == 0) return PSSO_OK;
+  if (c->swarm_fn) return swarm_run(c, t0, niter);
   int64_t done = 0;
   if (c->stream != nullptr && niter >= GRAPH_CHUNK && !c->profiling) {
     if (!c->graph) {  // capture GRAPH_CHUNK fused iterations, t read from t_dev
@@ -876,6 +992,7 @@ int psso_profile(psso_ctx* c, int32_t enable) {
   if (!c) return fail(nullptr, PSSO_E_INVALID, "null context");
   c->profiling = enable != 0;
   c->ev_used = 0;
+  c->prof_iters = 0;
   return PSSO_OK;
 }
 
@@ -889,8 +1006,9 @@ int psso_profile_read(psso_ctx* c, double* kernel_ms, int64_t* nlaunch) {
     tot += ms;
   }
   if (kernel_ms) *kernel_ms = tot;
-  if (nlaunch) *nlaunch = (int64_t)(c->ev_used / 2);
+  if (nlaunch) *nlaunch = c->prof_iters;
   c->ev_used = 0;
+  c->prof_iters = 0;
   return PSSO_OK;
 }
 

@@ -514,7 +514,7 @@ template <typename T, int V, int RNG>
 __device__ __forceinline__ VecT<T, V> search_chunk(const TileParams& p, const VecT<T, V>& x,
                                                    const VecT<T, V>& pb, const VecT<T, V>& gv,
                                                    uint64_t hr, uint64_t fr, int col, uint64_t gi,
-                                                   int64_t t) {
+                                                   int64_t t, uint64_t seed) {
   VecT<T, V> nv;
   if constexpr (RNG == 0) {
     uint64_t g = GAMMA * (uint64_t)(col + 1);
@@ -536,7 +536,7 @@ __device__ __forceinline__ VecT<T, V> search_chunk(const TileParams& p, const Ve
       const int j = col + v;
       if (v == 0 || (j & 1) == 0)
         w = philox4x32_10((uint32_t)(j >> 1), (uint32_t)gi, (uint32_t)(gi >> 32), (uint32_t)t,
-                          (uint32_t)p.seed, (uint32_t)(p.seed >> 32));
+                          (uint32_t)seed, (uint32_t)(seed >> 32));
       const uint64_t kb = w.w[j & 1];
       const double raw = __dmul_rn((double)w.w[2 + (j & 1)], 2.3283064365386963e-10);
       const double fresh = __dadd_rn(p.var_min, __dmul_rn(p.span, raw));
@@ -663,7 +663,7 @@ __global__ void __launch_bounds__(NT, PSSO_MINB) k_tile(const __grid_constant__ 
         } else if (mode & M_SEARCH) {
           const VecT<T, V> gv = *reinterpret_cast<const VecT<T, V>*>(gb + col);
           nv = search_chunk<T, V, RNG>(p, xv[u], pv[u], gv, RNG == 0 ? hbs[row] : 0,
-                                       RNG == 0 ? hfs[row] : 0, col, (uint64_t)(gi0 + row), t);
+                                       RNG == 0 ? hfs[row] : 0, col, (uint64_t)(gi0 + row), t, p.seed);
         } else {
           nv = xv[u];  // M_LOAD: evaluate existing positions
         }
@@ -867,7 +867,7 @@ __global__ void __launch_bounds__(NT, 2) k_fused(const __grid_constant__ TilePar
       const VecT<T, V> gv = *reinterpret_cast<const VecT<T, V>*>(gb + col);
       const VecT<T, V> nv = search_chunk<T, V, RNG>(p, xv, pv, gv, RNG == 0 ? hbs[row] : 0,
                                                    RNG == 0 ? hfs[row] : 0, col,
-                                                   (uint64_t)(gi0 + row), t);
+                                                   (uint64_t)(gi0 + row), t, p.seed);
       *reinterpret_cast<VecT<T, V>*>(Xs + e) = nv;
       stg_stream<T, V>(Xt + e, nv);
     }
@@ -985,8 +985,15 @@ __device__ __forceinline__ T chain_term1(T x, T nb, int e) {
 template <typename T, int M>
 __host__ __device__ constexpr int chain_row_stride() { return 8 * M * (int)sizeof(T); }
 
-// Per-launch constants of the chain step.
+// Per-launch constants of the chain step (per swarm in the batched kernel).
 struct ChainEnv {
+  void* X;                // rows x D positions / pbests of this swarm (shard)
+  void* P;
+  double* p_f;
+  double* sol_f;          // may be null
+  unsigned long long* bad;
+  int64_t row_lo;         // global index of local row 0
+  uint64_t seed;
   uint64_t rootb, rootf;  // keyed roots of the BRANCH/FRESH (or INIT) streams at t
   int64_t t;
   int D, n, mlen, tail;   // row length, terms, full chains, tail terms
@@ -1004,9 +1011,9 @@ __device__ __forceinline__ void chain_step(const TileParams& p, const ChainEnv& 
   using N = Num<T>;
   const int lane = threadIdx.x & 31, k = lane & 7, seg = lane & ~7;
   const int D = ev.D;
-  const int64_t gi = p.row_lo + r;
-  T* __restrict__ xr = reinterpret_cast<T*>(p.X) + r * (int64_t)D;
-  T* __restrict__ pr = reinterpret_cast<T*>(p.P) + r * (int64_t)D;
+  const int64_t gi = ev.row_lo + r;
+  T* __restrict__ xr = reinterpret_cast<T*>(ev.X) + r * (int64_t)D;
+  T* __restrict__ pr = reinterpret_cast<T*>(ev.P) + r * (int64_t)D;
   const int mode = INIT ? (M_INIT | M_EVAL | M_CAND | M_SOLF)
                         : (M_SEARCH | M_EVAL | M_PBEST | M_CAND | (p.mode & M_SOLF));
 
@@ -1024,7 +1031,7 @@ __device__ __forceinline__ void chain_step(const TileParams& p, const ChainEnv& 
           h = mix64(hb ^ g);
         } else {
           Philox4 w = philox4x32_10((uint32_t)(j >> 1), (uint32_t)gi, (uint32_t)(gi >> 32),
-                                    0xFFFFFFFFu, (uint32_t)p.seed, (uint32_t)(p.seed >> 32));
+                                    0xFFFFFFFFu, (uint32_t)ev.seed, (uint32_t)(ev.seed >> 32));
           const int s2 = (j & 1) * 2;
           h = ((uint64_t)w.w[s2] << 32) | w.w[s2 + 1];
         }
@@ -1061,7 +1068,7 @@ __device__ __forceinline__ void chain_step(const TileParams& p, const ChainEnv& 
         v = kb >= p.Kg ? (T)fresh : v;
       } else {
         VecT<T, 1> xv{{x[m]}}, pb{{pv[m]}}, gv{{gb[j]}};
-        v = search_chunk<T, 1, 1>(p, xv, pb, gv, 0, 0, j, (uint64_t)gi, ev.t).v[0];
+        v = search_chunk<T, 1, 1>(p, xv, pb, gv, 0, 0, j, (uint64_t)gi, ev.t, ev.seed).v[0];
       }
       x[m] = v;
       if (rv && (FULL || j < D)) stg_stream<T, 1>(xr + j, VecT<T, 1>{{v}});
@@ -1146,18 +1153,18 @@ __device__ __forceinline__ void chain_step(const TileParams& p, const ChainEnv& 
   // ---- bookkeeping (identical on the 8 lanes; lane k == 0 writes)
   if (rv) {
     if (k == 0) {
-      if (!isfinite(f) && p.bad)
-        atomicMin(p.bad, ((unsigned long long)(ev.t + 1) << 40) | (unsigned long long)gi);
-      if (p.sol_f && ((mode & M_SOLF) || !isfinite(f))) p.sol_f[r] = f;
+      if (!isfinite(f) && ev.bad)
+        atomicMin(ev.bad, ((unsigned long long)(ev.t + 1) << 40) | (unsigned long long)gi);
+      if (ev.sol_f && ((mode & M_SOLF) || !isfinite(f))) ev.sol_f[r] = f;
     }
     double pf = f;
     if (INIT) {
-      if (k == 0) p.p_f[r] = f;
+      if (k == 0) ev.p_f[r] = f;
     } else {
       const bool imp = f <= pf_row;  // parallel.py:109, ties refresh
       pf = imp ? f : pf_row;
       if (imp) {
-        if (k == 0) p.p_f[r] = f;
+        if (k == 0) ev.p_f[r] = f;
 #pragma unroll
         for (int m = 0; m < M; ++m) {
           const int j = k + 8 * m;
@@ -1213,6 +1220,13 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, PSSO_CHAIN_MINB)
   if (!INIT && p.bad && *(volatile unsigned long long*)p.bad != ~0ull) return;
 
   ChainEnv ev;
+  ev.X = p.X;
+  ev.P = p.P;
+  ev.p_f = p.p_f;
+  ev.sol_f = p.sol_f;
+  ev.bad = p.bad;
+  ev.row_lo = p.row_lo;
+  ev.seed = p.seed;
   ev.t = p.t_dev ? *p.t_dev : p.t_arg;
   ev.D = p.D;
   // FULL: D == 8*M, so the chain lengths and the tail are compile-time
@@ -1438,7 +1452,7 @@ __global__ void __launch_bounds__(256, 2) k_rows(const __grid_constant__ TilePar
         for (int m = 0; m < M; ++m) {
           const int j = jb + 8 * m;
           VecT<T, 1> xv{{x[m]}}, pb{{pv[m]}}, gv{{gbl[j]}};
-          x[m] = search_chunk<T, 1, 1>(p, xv, pb, gv, 0, 0, j, (uint64_t)gi, t).v[0];
+          x[m] = search_chunk<T, 1, 1>(p, xv, pb, gv, 0, 0, j, (uint64_t)gi, t, p.seed).v[0];
           stg_stream<T, 1>(xr + j, VecT<T, 1>{{x[m]}});
         }
       }

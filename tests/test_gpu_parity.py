@@ -469,3 +469,52 @@ def test_philox_mode_distribution_matches_reference():
     assert abs(gpu.mean() - ref.mean()) <= 0.10 * ref.mean(), (gpu.mean(), ref.mean())
     assert stats.kruskal(gpu, ref).pvalue > 0.01
     assert stats.ttest_ind(gpu, ref).pvalue > 0.01
+
+
+# ------------------------------------------- whole-run kernel (k_swarm) ----
+
+def _engine_run(fid, nsol, nvar, niter, monkeypatch, env=None, dtype="float64", rng="reference",
+                seed=3):
+    for k in ("PSSO_NO_SWARM", "PSSO_NO_CHAIN"):
+        monkeypatch.delenv(k, raising=False)
+    for k, v in (env or {}).items():
+        monkeypatch.setenv(k, v)
+    fn = _fn(fid, nvar)
+    p = _params(fn, nsol, niter)
+    eng = DeviceEngine(p, fn, seed, dtype=dtype, rng=rng, keep_sol_f=True)
+    try:
+        eng.initialize()
+        eng.run(0, 7)            # two launches: the loop state carries across calls
+        eng.run(7, niter - 7)
+        eng.check()
+        sw = eng.to_host()
+        traj = eng.traj.cpu().numpy()
+    finally:
+        eng.close()
+    return sw, traj
+
+
+@pytest.mark.parametrize("fid,nsol,nvar,niter", [
+    ("f1", 100, 30, 60),      # C1 shape: one CTA
+    ("f5", 1024, 100, 40),    # C2 shape: 32 CTAs and a swarm barrier
+    ("f7", 1024, 100, 30),    # sequential product through the smem rows
+    ("f4", 1001, 64, 30), ("f3", 333, 20, 30), ("f8", 515, 128, 30), ("f6", 4099, 33, 25),
+])
+def test_whole_run_kernel_matches_streaming_path(fid, nsol, nvar, niter, monkeypatch):
+    """k_swarm (one launch, swarm barrier) == fused+gBest launches per iteration, bitwise."""
+    a, ta = _engine_run(fid, nsol, nvar, niter, monkeypatch)
+    b, tb = _engine_run(fid, nsol, nvar, niter, monkeypatch, env={"PSSO_NO_SWARM": "1"})
+    assert np.array_equal(ta, tb)
+    for name in ("sol", "pbests", "gbest", "p_f"):
+        assert np.array_equal(getattr(a, name), getattr(b, name)), name
+    assert a.g_f == b.g_f
+
+
+@pytest.mark.parametrize("dtype,rng", [("float32", "reference"), ("float64", "philox"),
+                                       ("float32", "philox")])
+def test_whole_run_kernel_other_modes(dtype, rng, monkeypatch):
+    a, ta = _engine_run("f5", 1024, 100, 30, monkeypatch, dtype=dtype, rng=rng)
+    b, tb = _engine_run("f5", 1024, 100, 30, monkeypatch, env={"PSSO_NO_SWARM": "1"},
+                        dtype=dtype, rng=rng)
+    assert np.array_equal(ta, tb) and np.array_equal(a.gbest, b.gbest)
+    assert np.array_equal(a.sol, b.sol) and np.array_equal(a.pbests, b.pbests)
