@@ -106,8 +106,14 @@ int psso_init(psso_ctx* ctx);
 int psso_step(psso_ctx* ctx, int64_t t);
 
 /* replaces: the whole loop `for t in range(t0, t0+niter)` (parallel.py:192-212).
- * Asynchronous; the iterations are replayed from a captured CUDA graph. */
+ * Asynchronous.  Swarms of up to 2^22 elements run all iterations in ONE
+ * persistent launch (k_swarm, swarm barrier per iteration); larger swarms
+ * replay the fused + gBest kernel pair from a captured CUDA graph. */
 int psso_run(psso_ctx* ctx, int64_t t0, int64_t niter);
+
+/* Name of the iteration kernel psso_run uses for this configuration
+ * (k_swarm / k_chain / k_rows / k_fused / k_tile with its template arguments). */
+const char* psso_kernel_name(const psso_ctx* ctx);
 
 /* Phase API -- replaces search_phase / evaluate_phase / update_pbests_phase /
  * update_gbest_phase (parallel.py:120-144).  `t < 0` in psso_evaluate means
@@ -139,10 +145,11 @@ int psso_check(psso_ctx* ctx, int64_t* bad_t, int64_t* bad_i);
 int64_t psso_launch_count(const psso_ctx* ctx);
 
 /* Kernel timing for the roofline: while enabled, psso_step / psso_run (which
- * then launches directly instead of replaying its graph) bracket every fused
- * tile-kernel launch with CUDA events on the context's stream.
+ * then launches directly instead of replaying its graph) bracket every
+ * iteration-kernel launch with CUDA events on the context's stream.
  * psso_profile_read synchronizes, returns the summed kernel time (ms) and the
- * number of timed launches, and resets the record. */
+ * number of iterations those launches covered (one per fused launch, niter per
+ * whole-run launch), and resets the record. */
 int psso_profile(psso_ctx* ctx, int32_t enable);
 int psso_profile_read(psso_ctx* ctx, double* kernel_ms, int64_t* nlaunch);
 
@@ -162,6 +169,17 @@ int psso_eval_rows(int32_t fn_id, int32_t dtype, int64_t nvar, const void* x, in
  * back, frees.  wall_s = loop-only device time (parallel.py:190,216). */
 int psso_solve(const psso_config* cfg, int64_t niter, double* traj, void* best_position,
                double* best_fitness, double* wall_s);
+
+/* replaces: the reference's multi-seed protocol -- one run_parallel per seed
+ * (harness.py:148-163, 217-263: seed = base_seed + run_id) -- as ONE device
+ * job: nseeds independent swarms of cfg (cfg->seed ignored), each with its own
+ * keyed RNG seed, run side by side by the whole-run kernel.  Per swarm the
+ * results are bit-identical to psso_solve with that seed.  Outputs (host):
+ * traj nseeds x niter, best_position nseeds x nvar (dtype), best_fitness
+ * nseeds.  wall_s = loop-only device time of the whole batch.  Needs
+ * nvar <= 128 and nsol*nvar <= 2^22 (else PSSO_E_UNSUPPORTED). */
+int psso_solve_batch(const psso_config* cfg, const uint64_t* seeds, int32_t nseeds, int64_t niter,
+                     double* traj, void* best_position, double* best_fitness, double* wall_s);
 
 #ifdef __cplusplus
 }

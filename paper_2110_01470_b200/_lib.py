@@ -32,6 +32,7 @@ EXPORTS = (
     "psso_update_pbests", "psso_update_gbest", "psso_candidate_bytes", "psso_init_local",
     "psso_step_local", "psso_apply_candidates", "psso_check", "psso_launch_count",
     "psso_rng_uniform", "psso_eval_rows", "psso_solve", "psso_profile", "psso_profile_read",
+    "psso_kernel_name", "psso_solve_batch",
 )
 
 
@@ -116,6 +117,9 @@ def load():
     L.psso_rng_uniform.argtypes = [u64, u64, u64, vp, vp, i64, vp, vp]
     L.psso_eval_rows.argtypes = [i32, i32, i64, vp, i64, vp, dbl, vp]
     L.psso_solve.argtypes = [cfgp, i64, vp, vp, ctypes.POINTER(dbl), ctypes.POINTER(dbl)]
+    L.psso_solve_batch.argtypes = [cfgp, vp, i32, i64, vp, vp, vp, ctypes.POINTER(dbl)]
+    L.psso_kernel_name.argtypes = [vp]
+    L.psso_kernel_name.restype = ctypes.c_char_p
     for name in EXPORTS:
         if not hasattr(L, name):
             raise RuntimeError(f"{LIB_PATH} does not export {name}")

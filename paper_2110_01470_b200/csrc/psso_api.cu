@@ -373,6 +373,7 @@ struct psso_ctx {
   int64_t* sw_slot_i;
   void* sw_slot_row;
   uint64_t* sw_seed;
+  std::string kname;     // the iteration kernel psso_run launches (psso_kernel_name)
   std::string err;
 };
 
@@ -540,6 +541,8 @@ extern "C" {
 
 const char* psso_version(void) { return "psso-b200 1 (sm_100a)"; }
 
+const char* psso_kernel_name(const psso_ctx* ctx) { return ctx ? ctx->kname.c_str() : ""; }
+
 const char* psso_last_error(const psso_ctx* ctx) {
   if (ctx && !ctx->err.empty()) return ctx->err.c_str();
   return g_err.c_str();
@@ -698,6 +701,22 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
         c->swarm_G = (int)std::max<int64_t>(1, std::min<int64_t>(want, cap));
       }
     }
+  }
+  {
+    const char* tn = cfg->dtype == PSSO_F64 ? "double" : "float";
+    const char* rn = cfg->rng_mode == PSSO_RNG_REFERENCE ? "ref" : "philox";
+    const int64_t D = cfg->nvar;
+    const int M = D <= 32 ? 4 : D <= 64 ? 8 : 16;
+    char b[160];
+    if (c->swarm_fn)
+      std::snprintf(b, sizeof b, "k_swarm<%s,f%d,%s,M=%d> x%d CTAs", tn, cfg->fn_id, rn, M, c->swarm_G);
+    else if (c->rows_w)
+      std::snprintf(b, sizeof b, "k_rows<%s,f%d,%s,W=%d>", tn, cfg->fn_id, rn, c->rows_w);
+    else if (c->chain)
+      std::snprintf(b, sizeof b, "k_chain<%s,f%d,%s,M=%d%s>", tn, cfg->fn_id, rn, M, D == 8 * M ? ",full" : "");
+    else
+      std::snprintf(b, sizeof b, "%s<%s,f%d,%s>", c->LF.V > 1 ? "k_fused" : "k_tile", tn, cfg->fn_id, rn);
+    c->kname = b;
   }
   c->argmin_grid = (int)std::min<int64_t>((rows + 255) / 256, 4 * c->num_sms);
   c->nslots = std::max(std::max(std::max(c->grid, c->fused_grid), c->init_grid), c->argmin_grid);
@@ -1119,6 +1138,122 @@ int psso_solve(const psso_config* cfg, int64_t niter, double* traj, void* best_p
   if (wall_s) *wall_s = ms * 1e-3;
   cleanup();
   if (e != cudaSuccess) return cuda_fail(nullptr, e, "psso_solve copy-back");
+  return PSSO_OK;
+}
+
+int psso_solve_batch(const psso_config* cfg, const uint64_t* seeds, int32_t nseeds, int64_t niter,
+                     double* traj, void* best_position, double* best_fitness, double* wall_s) {
+  std::string err;
+  int rc = validate(cfg, err);
+  if (rc) return fail(nullptr, rc, err);
+  if (niter < 1) return fail(nullptr, PSSO_E_INVALID, "niter must be a positive integer");
+  if (nseeds < 1 || !seeds) return fail(nullptr, PSSO_E_INVALID, "need at least one seed");
+  if (cfg->row_lo != 0 || cfg->row_hi != cfg->nsol) return fail(nullptr, PSSO_E_INVALID, "psso_solve_batch runs whole swarms");
+  psso_ctx* c = nullptr;
+  if ((rc = psso_create(cfg, &c)) != PSSO_OK) return rc;
+  if (!c->swarm_fn) {
+    psso_destroy(c);
+    return fail(nullptr, PSSO_E_UNSUPPORTED, "batched runs need nvar <= 128 and nsol*nvar <= 2^22 (whole-run kernel)");
+  }
+  const size_t es = cfg->dtype == PSSO_F64 ? 8 : 4;
+  const size_t B = (size_t)nseeds, N = (size_t)cfg->nsol, D = (size_t)cfg->nvar;
+  // CTAs per swarm: the single-swarm choice when the whole batch is co-resident,
+  // else one CTA per swarm (no grid barrier, any batch size)
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, c->swarm_fn, NT, c->swarm_smem);
+  if (e != cudaSuccess) { psso_destroy(c); return cuda_fail(nullptr, e, "occupancy"); }
+  const int64_t cap = (int64_t)per_sm * c->num_sms;
+  int G = c->swarm_G;
+  if ((int64_t)G * (int64_t)B > cap) G = (int)std::max<int64_t>(1, cap / (int64_t)B);
+  if ((int64_t)G * (int64_t)B > cap) G = 1;
+  struct Buf { void* p = nullptr; } X, P, pf, gb, gf, tr, bar, sf, si, sr, sd, bad;
+  cudaStream_t s = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  auto cleanup = [&]() {
+    for (Buf* b : {&X, &P, &pf, &gb, &gf, &tr, &bar, &sf, &si, &sr, &sd, &bad}) cudaFree(b->p);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    if (s) cudaStreamDestroy(s);
+    psso_destroy(c);
+  };
+  if ((e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaEventCreate(&e0)) != cudaSuccess || (e = cudaEventCreate(&e1)) != cudaSuccess ||
+      (e = cudaMalloc(&X.p, B * N * D * es)) != cudaSuccess ||
+      (e = cudaMalloc(&P.p, B * N * D * es)) != cudaSuccess ||
+      (e = cudaMalloc(&pf.p, B * N * 8)) != cudaSuccess ||
+      (e = cudaMalloc(&gb.p, B * D * es)) != cudaSuccess ||
+      (e = cudaMalloc(&gf.p, B * 8)) != cudaSuccess ||
+      (e = cudaMalloc(&tr.p, B * (size_t)niter * 8)) != cudaSuccess ||
+      (e = cudaMalloc(&bar.p, B * sizeof(unsigned int))) != cudaSuccess ||
+      (e = cudaMalloc(&sf.p, B * 2 * G * 8)) != cudaSuccess ||
+      (e = cudaMalloc(&si.p, B * 2 * G * 8)) != cudaSuccess ||
+      (e = cudaMalloc(&sr.p, B * 2 * G * D * es)) != cudaSuccess ||
+      (e = cudaMalloc(&sd.p, B * 8)) != cudaSuccess ||
+      (e = cudaMalloc(&bad.p, B * 8)) != cudaSuccess ||
+      (e = cudaMemcpy(sd.p, seeds, B * 8, cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemset(bad.p, 0xff, B * 8)) != cudaSuccess) {
+    cleanup();
+    return cuda_fail(nullptr, e, "psso_solve_batch alloc");
+  }
+  psso_buffers pb;
+  std::memset(&pb, 0, sizeof pb);
+  pb.sol = X.p; pb.pbests = P.p; pb.p_f = (double*)pf.p; pb.gbest = gb.p; pb.g_f = (double*)gf.p;
+  c->buf = pb;
+  c->stream = s;
+  c->bound = true;
+  TileParams p = tile_params(c, fused_mode(c), 0, nullptr, true);
+  p.off_bar = c->swarm_off_bar;
+  p.off_scr = c->swarm_off_scr;
+  SwarmParams sp;
+  std::memset(&sp, 0, sizeof sp);
+  sp.rows = (int64_t)N;
+  sp.G = G;
+  sp.bar = (unsigned int*)bar.p;
+  sp.slot_f = (double*)sf.p;
+  sp.slot_i = (int64_t*)si.p;
+  sp.slot_row = sr.p;
+  sp.traj = (double*)tr.p;
+  sp.traj_stride = niter;
+  sp.g_f = (double*)gf.p;
+  sp.gbest = gb.p;
+  sp.seeds = (const uint64_t*)sd.p;
+  sp.bad = (unsigned long long*)bad.p;
+  auto launch = [&]() -> cudaError_t {
+    cudaError_t r = cudaMemsetAsync(bar.p, 0, B * sizeof(unsigned int), s);
+    if (r != cudaSuccess) return r;
+    void* args[] = {(void*)&p, (void*)&sp};
+    if (G > 1) return cudaLaunchCooperativeKernel(c->swarm_fn, dim3(G, (unsigned)B), dim3(NT), args, c->swarm_smem, s);
+    return cudaLaunchKernel(c->swarm_fn, dim3(1, (unsigned)B), dim3(NT), args, c->swarm_smem, s);
+  };
+  sp.do_init = 1;  // initialize (core.py:196-210), outside the timed loop (parallel.py:190)
+  sp.niter = 0;
+  if ((e = launch()) != cudaSuccess) { cleanup(); return cuda_fail(nullptr, e, "psso_solve_batch init"); }
+  sp.do_init = 0;
+  sp.t0 = 0;
+  sp.niter = niter;
+  cudaEventRecord(e0, s);
+  if ((e = launch()) != cudaSuccess) { cleanup(); return cuda_fail(nullptr, e, "psso_solve_batch run"); }
+  cudaEventRecord(e1, s);
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) { cleanup(); return cuda_fail(nullptr, e, "psso_solve_batch"); }
+  std::vector<unsigned long long> bk(B);
+  e = cudaMemcpy(bk.data(), bad.p, B * 8, cudaMemcpyDeviceToHost);
+  for (size_t q = 0; e == cudaSuccess && q < B; ++q)
+    if (bk[q] != ~0ull) {
+      const int64_t bt = (int64_t)(bk[q] >> 40) - 1, bi = (int64_t)(bk[q] & ((1ull << 40) - 1));
+      g_err = "non-finite fitness in swarm " + std::to_string(q) + " (seed " + std::to_string(seeds[q]) +
+              ") at particle " + std::to_string(bi) +
+              (bt < 0 ? std::string(" during initialization") : " at iteration " + std::to_string(bt));
+      cleanup();
+      return PSSO_E_NONFINITE;
+    }
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  if (e == cudaSuccess && traj) e = cudaMemcpy(traj, tr.p, B * (size_t)niter * 8, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && best_position) e = cudaMemcpy(best_position, gb.p, B * D * es, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && best_fitness) e = cudaMemcpy(best_fitness, gf.p, B * 8, cudaMemcpyDeviceToHost);
+  if (wall_s) *wall_s = ms * 1e-3;
+  cleanup();
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "psso_solve_batch copy-back");
   return PSSO_OK;
 }
 

@@ -20,7 +20,7 @@
 // __syncthreads only.  blockIdx.y indexes independent swarms (seeds) of a
 // batch -- the reference's multi-seed protocol (harness.py:217-263) as one
 // launch.  The same keyed RNG and numpy-order fitness as the streaming path,
-// so results are bit-identical to it and to the oracle.
+// so results are bit-identical to it.
 #pragma once
 
 #include "psso_device.cuh"

@@ -33,6 +33,7 @@ __all__ = [
     "update_pbests_phase",
     "update_gbest_phase",
     "run_parallel",
+    "run_parallel_batch",
 ]
 
 
@@ -207,3 +208,59 @@ def run_parallel(
         best_position=best_position,
         trajectory=trajectory,
     )
+
+
+def run_parallel_batch(
+    params: SsoParams,
+    f,
+    seeds,
+    *,
+    dtype: str = "float64",
+    rng: str = "reference",
+    run_id_base: int = 0,
+) -> list:
+    """Many independent runs of ``run_parallel`` (one per seed) as one device job.
+
+    The reference's experiment protocol runs the same configuration for many
+    seeds (harness.py:148-163, 217-263, seed = base_seed + run_id); here all
+    swarms run side by side in one whole-run kernel launch (psso_solve_batch).
+    Record k is bit-identical to ``run_parallel(params, f, seeds[k])``;
+    ``wall_time_s`` is the loop-only device time of the whole batch.  Needs
+    ``nvar <= 128`` and ``nsol * nvar <= 2**22``.
+    """
+    import ctypes
+
+    from . import _lib
+    from .core import NonFiniteFitnessError
+    from .engine import make_config
+
+    seeds = [int(s) for s in seeds]
+    if not seeds:
+        raise ValueError("need at least one seed")
+    _lib.require_device()
+    L = _lib.load()
+    cfg = make_config(params, f, seeds[0], dtype=dtype, rng=rng)
+    B, n, D = len(seeds), params.niter, params.nvar
+    arr = (ctypes.c_uint64 * B)(*[s & ((1 << 64) - 1) for s in seeds])
+    traj = np.empty((B, n), dtype=np.float64)
+    best = np.empty((B, D), dtype=np.float64 if dtype == "float64" else np.float32)
+    bestf = np.empty(B, dtype=np.float64)
+    wall = ctypes.c_double()
+    rc = L.psso_solve_batch(ctypes.byref(cfg), arr, B, n, traj.ctypes.data, best.ctypes.data,
+                            bestf.ctypes.data, ctypes.byref(wall))
+    if rc == _lib.PSSO_E_NONFINITE:  # "... at particle I (during initialization | at iteration T)"
+        import re
+
+        msg = _lib.last_error()
+        m = re.search(r"particle (\d+)(?: at iteration (\d+))?", msg)
+        it = None if m is None or m.group(2) is None else int(m.group(2))
+        raise NonFiniteFitnessError(float("nan"), int(m.group(1)) if m else -1, it)
+    _lib.check(rc)
+    return [
+        RunRecord(run_id=run_id_base + k, schedule=ScheduleKind.PARALLEL,
+                  function=getattr(f, "id", "custom"), nsol=params.nsol, nvar=D, niter=n,
+                  cw=params.cw, cp=params.cp, cg=params.cg, seed=seeds[k],
+                  best_fitness=float(bestf[k]), wall_time_s=wall.value,
+                  best_position=best[k].astype(np.float64), trajectory=traj[k].copy())
+        for k in range(B)
+    ]

@@ -518,3 +518,41 @@ def test_whole_run_kernel_other_modes(dtype, rng, monkeypatch):
                         dtype=dtype, rng=rng)
     assert np.array_equal(ta, tb) and np.array_equal(a.gbest, b.gbest)
     assert np.array_equal(a.sol, b.sol) and np.array_equal(a.pbests, b.pbests)
+
+
+# ------------------------------------------------ multi-seed batch runs ----
+
+@pytest.mark.parametrize("fid,nsol,nvar,niter,nseeds", [
+    ("f1", 100, 30, 200, 5),    # C1 shape, co-resident swarms with a swarm barrier each
+    ("f5", 1024, 100, 30, 3),   # C2 shape
+    ("f7", 256, 100, 20, 4),
+    ("f4", 60, 16, 50, 300),    # more swarms than co-resident CTAs: one CTA per swarm
+])
+def test_batch_runs_equal_single_runs(fid, nsol, nvar, niter, nseeds):
+    fn = _fn(fid, nvar)
+    p = _params(fn, nsol, niter)
+    seeds = [11 + 7 * k for k in range(nseeds)]
+    recs = psso.run_parallel_batch(p, fn, seeds)
+    assert [r.seed for r in recs] == seeds and [r.run_id for r in recs] == list(range(nseeds))
+    for k in sorted({0, nseeds // 2, nseeds - 1}):
+        one = psso.run_parallel(p, fn, seeds[k])
+        assert np.array_equal(recs[k].trajectory, one.trajectory)
+        assert np.array_equal(recs[k].best_position, one.best_position)
+        assert recs[k].best_fitness == one.best_fitness
+
+
+def test_batch_c1_appendix_values():
+    """Config C1 for seeds 0 and 1 in one launch: the reference's final values bitwise."""
+    fn = _fn("f1", 30)
+    p = _params(fn, 100, 1000)
+    r0, r1 = psso.run_parallel_batch(p, fn, [0, 1])
+    assert r0.best_fitness == 8.542836016810329
+    assert r1.best_fitness == 8.834077304158543
+
+
+def test_batch_nonfinite_names_particle():
+    fn = psso.probe_function(8, level=0.999, bounds=(-1.0, 1.0))  # +inf once x[0] > 0.999
+    p = _params(fn, 64, 400)
+    with pytest.raises(psso.NonFiniteFitnessError) as ei:
+        psso.run_parallel_batch(p, fn, [0, 1, 2])
+    assert ei.value.particle >= 0
