@@ -41,15 +41,31 @@ L2_BYTES = 126 * 1024 * 1024
 
 WORKLOADS = {
     # name: (fid, nsol per rank, nvar, dtype, BASELINE config)
+    "c1": ("f1", 100, 30, "float64", "C1 Sphere N=100 Nvar=30 fp64"),
     "c3": ("f5", 1 << 20, 128, "float64", "C3 Rastrigin N=2^20 Nvar=128 fp64"),
     "c3f32": ("f5", 1 << 20, 128, "float32", "C3 Rastrigin N=2^20 Nvar=128 fp32"),
     "c4": ("f4", 1 << 24, 64, "float64", "C4 Rosenbrock N=2^24 Nvar=64 fp64"),
     "c5": ("f6", 65536, 4096, "float64", "C5 Ackley N=65536 Nvar=4096 fp64"),
     "c2": ("f5", 1024, 100, "float64", "C2 Rastrigin N=1024 Nvar=100 fp64"),
+    "c2f4": ("f4", 1024, 100, "float64", "C2 Rosenbrock N=1024 Nvar=100 fp64"),
+    "c2f6": ("f6", 1024, 100, "float64", "C2 Ackley N=1024 Nvar=100 fp64"),
+    "c2f7": ("f7", 1024, 100, "float64", "C2 Griewank N=1024 Nvar=100 fp64"),
     # diagnostics (not BASELINE configs): C3 shape with the cheapest objective
     "c3sphere": ("f1", 1 << 20, 128, "float64", "diagnostic: Sphere N=2^20 Nvar=128 fp64"),
     "c3sphere32": ("f1", 1 << 20, 128, "float32", "diagnostic: Sphere N=2^20 Nvar=128 fp32"),
 }
+
+
+def _traffic(workload, kernel):
+    """DRAM bytes per launch of this workload's kernel from the committed ncu capture
+    (bench_traffic.json, written by scripts/ncu_summary.py traffic), else None."""
+    p = ROOT / "bench_traffic.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text()).get(workload)
+    if not d or d.get("kernel") != kernel:
+        return None
+    return d["dram_bytes_per_launch"]
 
 
 def _peaks():
@@ -233,6 +249,7 @@ def run_ours(args, wl):
     if ws > 1:
         dist.barrier()
     launches = eng.launches - l0
+    kname = L.psso_kernel_name(eng.ctx).decode()
     kms, kn = ctypes.c_double(), ctypes.c_int64()
     _lib.check(L.psso_profile_read(eng.ctx, ctypes.byref(kms), ctypes.byref(kn)))
     L.psso_profile(eng.ctx, 0)
@@ -244,7 +261,7 @@ def run_ours(args, wl):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, kern_ms = float(t[0]), float(t[1])
     else:
-        kern_ms = kms.value / max(kn.value, 1)
+        kern_ms = kms.value / max(kn.value, 1)  # per iteration
     eng.close()
     del eng
     torch.cuda.empty_cache()
@@ -299,10 +316,12 @@ def run_ours(args, wl):
                    "parallelism": f"particle shards x{ws}" + (" + NCCL all-gather of gBest "
                                                              "candidates per iteration" if ws > 1 else "")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
-                     "kernel": "k_tile<%s,%s,%s>" % ("double" if es == 8 else "float", fid, args.rng),
-                     "kernel_ms": kern_ms, "alg_bytes_per_launch": alg_bytes,
-                     "alg_bytes_per_pvu": 3 * es},
+                     "frac": achieved / peak, "traffic": _traffic(wl, kname), "peak_source": peak_src,
+                     "kernel": kname, "kernel_ms_per_iteration": kern_ms,
+                     "alg_bytes_per_launch": alg_bytes, "alg_bytes_per_pvu": 3 * es,
+                     "note": ("per iteration: one fused launch (streaming path)" if "k_swarm" not in kname
+                              else "whole-run kernel: all timed iterations in one launch; L2/SMEM-"
+                                   "resident swarm, so the HBM roofline does not bind")},
         "gpu_launches": launches,
         "clocks": clocks,
         "e2e": e2e,

@@ -365,12 +365,14 @@ struct psso_ctx {
   int64_t prof_iters;    // iterations covered by the timed launches
   // whole-run kernel for small swarms (psso_swarm.cuh); null: streaming path
   const void* swarm_fn;
-  int swarm_G;
+  int swarm_G, swarm_gpc;
+  bool swarm_res;
   size_t swarm_smem;
-  int swarm_off_bar, swarm_off_scr;
-  unsigned int* sw_bar;
+  int swarm_off_bar, swarm_off_scr, swarm_off_xs;
+  unsigned int* sw_epoch;
   double* sw_slot_f;
   int64_t* sw_slot_i;
+  int32_t* sw_slot_new;
   void* sw_slot_row;
   uint64_t* sw_seed;
   std::string kname;     // the iteration kernel psso_run launches (psso_kernel_name)
@@ -533,6 +535,63 @@ int fused_step(psso_ctx* c, int64_t t, int64_t* t_dev) {
   return launch_gbest(c, gb_params(c, t, t_dev, 0, c->fused_grid));
 }
 
+// Launch plan of the whole-run kernel for B swarms of this configuration:
+// RES (rows in smem, gpc row groups per CTA) when the tiles fit and the
+// B x G CTAs can be co-resident; else rows in HBM, one row group per warp.
+// G = 1 needs no co-residency (the swarm barrier is __syncthreads).
+struct SwarmPlan {
+  const void* fn = nullptr;
+  int G = 0, gpc = 0;
+  bool res = false;
+  size_t smem = 0;
+  int off_bar = 0, off_scr = 0, off_xs = 0;
+};
+
+bool plan_swarm(psso_ctx* c, int64_t B, SwarmPlan& sp, cudaError_t& e) {
+  const psso_config* cfg = &c->cfg;
+  const int64_t rows = cfg->row_hi - cfg->row_lo, D = cfg->nvar;
+  const int M = D <= 32 ? 4 : D <= 64 ? 8 : 16;
+  const int es = cfg->dtype == PSSO_F64 ? 8 : 4;
+  const int nw = NT / 32;
+  const bool smem_fn = cfg->fn_id == 3 || cfg->fn_id == 7 || cfg->fn_id == 8;
+  const int64_t ngroups = (rows + 3) / 4;
+  sp.off_bar = (int)align16((size_t)c->LF.off_red + 128 + 64 * M);
+  sp.off_scr = (int)align16((size_t)sp.off_bar + 64);
+  sp.off_xs = (int)align16((size_t)sp.off_scr + (smem_fn ? (size_t)nw * 4 * (8 * M) * es : 0));
+  e = cudaSuccess;
+  auto try_plan = [&](bool res, int64_t gpc, int64_t G) -> bool {
+    const size_t smem = res ? (size_t)sp.off_xs + (size_t)gpc * 4 * (D * 2 * es + 8) : (size_t)sp.off_xs;
+    if (smem > 227 * 1024) return false;
+    const void* f = swarm_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, M, res);
+    if (!f) return false;
+    int per_sm = 0;
+    if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess ||
+        (e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, NT, smem)) != cudaSuccess)
+      return false;
+    const int64_t cap = (int64_t)per_sm * c->num_sms;
+    if (per_sm < 1 || (G > 1 && G * B > cap)) return false;
+    sp.fn = f; sp.G = (int)G; sp.gpc = (int)gpc; sp.res = res; sp.smem = smem;
+    return true;
+  };
+  const char* g = std::getenv("PSSO_SWARM_GPC");
+  const int64_t gpc = std::max<int64_t>(1, std::min<int64_t>(ngroups, g && *g ? std::atoll(g) : nw));
+  if (try_plan(true, gpc, (ngroups + gpc - 1) / gpc)) return true;   // resident, co-resident
+  if (e != cudaSuccess) return false;
+  if (try_plan(true, ngroups, 1)) return true;                       // resident, one CTA per swarm
+  if (e != cudaSuccess) return false;
+  int per_sm = 0;                                                     // rows in HBM
+  const void* f = swarm_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, M, false);
+  if (!f) return false;
+  if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.off_xs)) != cudaSuccess ||
+      (e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, NT, sp.off_xs)) != cudaSuccess || per_sm < 1)
+    return false;
+  const int64_t cap = (int64_t)per_sm * c->num_sms;
+  int64_t G = std::max<int64_t>(1, std::min<int64_t>((ngroups + nw - 1) / nw, cap / B));
+  if (G * B > cap) G = 1;
+  sp.fn = f; sp.G = (int)G; sp.gpc = nw; sp.res = false; sp.smem = sp.off_xs;
+  return true;
+}
+
 }  // namespace
 
 // ------------------------------------------------------------- C ABI ----
@@ -677,28 +736,21 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
   if (c->chain && cfg->row_lo == 0 && cfg->row_hi == cfg->nsol &&
       rows * cfg->nvar <= PSSO_SWARM_MAX_ELEMS) {  // small swarm: the whole run in one launch
     const char* off = std::getenv("PSSO_NO_SWARM");
-    const int64_t D = cfg->nvar;
-    const int M = D <= 32 ? 4 : D <= 64 ? 8 : 16;
-    const void* f = (off && *off && *off != '0') ? nullptr : swarm_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, M);
-    if (f) {
-      const int es = cfg->dtype == PSSO_F64 ? 8 : 4;
-      const bool smem_fn = cfg->fn_id == 3 || cfg->fn_id == 7 || cfg->fn_id == 8;
-      // gbest | reduction + xs30 table (as k_chain) | winner record | smem rows
-      c->swarm_off_bar = (int)align16((size_t)c->LF.off_red + 128 + 64 * M);
-      c->swarm_off_scr = (int)align16((size_t)c->swarm_off_bar + 32);
-      c->swarm_smem = (size_t)c->swarm_off_scr + (smem_fn ? (size_t)(NT / 32) * 4 * (8 * M) * es : 0);
-      int per_sm_sw = 0;
-      if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->swarm_smem)) != cudaSuccess ||
-          (e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_sw, f, NT, c->swarm_smem)) != cudaSuccess) {
+    SwarmPlan sp;
+    if (!(off && *off && *off != '0')) {
+      if (!plan_swarm(c, 1, sp, e) && e != cudaSuccess) {
         delete c;
         return cuda_fail(nullptr, e, "psso_create swarm kernel");
       }
-      const int64_t groups = (rows + 3) / 4;
-      const int64_t want = (groups + (NT / 32) - 1) / (NT / 32);  // one row group per warp
-      const int64_t cap = (int64_t)per_sm_sw * c->num_sms;
-      if (per_sm_sw >= 1) {
-        c->swarm_fn = f;
-        c->swarm_G = (int)std::max<int64_t>(1, std::min<int64_t>(want, cap));
+      if (sp.fn) {
+        c->swarm_fn = sp.fn;
+        c->swarm_G = sp.G;
+        c->swarm_gpc = sp.gpc;
+        c->swarm_res = sp.res;
+        c->swarm_smem = sp.smem;
+        c->swarm_off_bar = sp.off_bar;
+        c->swarm_off_scr = sp.off_scr;
+        c->swarm_off_xs = sp.off_xs;
       }
     }
   }
@@ -709,7 +761,8 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
     const int M = D <= 32 ? 4 : D <= 64 ? 8 : 16;
     char b[160];
     if (c->swarm_fn)
-      std::snprintf(b, sizeof b, "k_swarm<%s,f%d,%s,M=%d> x%d CTAs", tn, cfg->fn_id, rn, M, c->swarm_G);
+      std::snprintf(b, sizeof b, "k_swarm<%s,f%d,%s,M=%d%s> x%d CTAs", tn, cfg->fn_id, rn, M,
+                    c->swarm_res ? ",smem-resident" : "", c->swarm_G);
     else if (c->rows_w)
       std::snprintf(b, sizeof b, "k_rows<%s,f%d,%s,W=%d>", tn, cfg->fn_id, rn, c->rows_w);
     else if (c->chain)
@@ -735,9 +788,10 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
     const size_t es = cfg->dtype == PSSO_F64 ? 8 : 4;
     const size_t G = (size_t)c->swarm_G;
     const uint64_t seed = cfg->seed;
-    if ((e = cudaMalloc(&c->sw_bar, sizeof(unsigned int))) != cudaSuccess ||
+    if ((e = cudaMalloc(&c->sw_epoch, 2 * G * sizeof(unsigned int))) != cudaSuccess ||
         (e = cudaMalloc(&c->sw_slot_f, 2 * G * sizeof(double))) != cudaSuccess ||
         (e = cudaMalloc(&c->sw_slot_i, 2 * G * sizeof(int64_t))) != cudaSuccess ||
+        (e = cudaMalloc(&c->sw_slot_new, 2 * G * sizeof(int32_t))) != cudaSuccess ||
         (e = cudaMalloc(&c->sw_slot_row, 2 * G * (size_t)cfg->nvar * es)) != cudaSuccess ||
         (e = cudaMalloc(&c->sw_seed, sizeof(uint64_t))) != cudaSuccess ||
         (e = cudaMemcpy(c->sw_seed, &seed, sizeof seed, cudaMemcpyHostToDevice)) != cudaSuccess) {
@@ -769,7 +823,8 @@ void psso_destroy(psso_ctx* c) {
   cudaFree(c->bad);
   cudaFree(c->t_dev);
   cudaFree(c->aux);
-  cudaFree(c->sw_bar);
+  cudaFree(c->sw_epoch);
+  cudaFree(c->sw_slot_new);
   cudaFree(c->sw_slot_f);
   cudaFree(c->sw_slot_i);
   cudaFree(c->sw_slot_row);
@@ -823,16 +878,19 @@ static int swarm_run(psso_ctx* c, int64_t t0, int64_t niter) {
   TileParams p = tile_params(c, fused_mode(c), t0, nullptr, true);
   p.off_bar = c->swarm_off_bar;
   p.off_scr = c->swarm_off_scr;
+  p.off_xs = c->swarm_off_xs;
   SwarmParams sp;
   std::memset(&sp, 0, sizeof sp);
   sp.t0 = t0;
   sp.niter = niter;
   sp.rows = c->cfg.row_hi - c->cfg.row_lo;
   sp.G = c->swarm_G;
+  sp.gpc = c->swarm_gpc;
   sp.do_init = 0;
-  sp.bar = c->sw_bar;
+  sp.epoch = c->sw_epoch;
   sp.slot_f = c->sw_slot_f;
   sp.slot_i = c->sw_slot_i;
+  sp.slot_new = c->sw_slot_new;
   sp.slot_row = c->sw_slot_row;
   sp.traj = c->buf.traj;
   sp.traj_stride = 0;
@@ -841,7 +899,7 @@ static int swarm_run(psso_ctx* c, int64_t t0, int64_t niter) {
   sp.seeds = c->sw_seed;
   sp.sol_f = c->buf.sol_f;
   sp.bad = c->bad;
-  CK(c, cudaMemsetAsync(c->sw_bar, 0, sizeof(unsigned int), c->stream));
+  CK(c, cudaMemsetAsync(c->sw_epoch, 0, 2 * (size_t)c->swarm_G * sizeof(unsigned int), c->stream));
   const bool timed = c->profiling;
   if (timed) {
     if (c->ev_used + 2 > c->ev.size()) {
@@ -1157,20 +1215,19 @@ int psso_solve_batch(const psso_config* cfg, const uint64_t* seeds, int32_t nsee
   }
   const size_t es = cfg->dtype == PSSO_F64 ? 8 : 4;
   const size_t B = (size_t)nseeds, N = (size_t)cfg->nsol, D = (size_t)cfg->nvar;
-  // CTAs per swarm: the single-swarm choice when the whole batch is co-resident,
-  // else one CTA per swarm (no grid barrier, any batch size)
-  int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, c->swarm_fn, NT, c->swarm_smem);
-  if (e != cudaSuccess) { psso_destroy(c); return cuda_fail(nullptr, e, "occupancy"); }
-  const int64_t cap = (int64_t)per_sm * c->num_sms;
-  int G = c->swarm_G;
-  if ((int64_t)G * (int64_t)B > cap) G = (int)std::max<int64_t>(1, cap / (int64_t)B);
-  if ((int64_t)G * (int64_t)B > cap) G = 1;
-  struct Buf { void* p = nullptr; } X, P, pf, gb, gf, tr, bar, sf, si, sr, sd, bad;
+  SwarmPlan pl;
+  cudaError_t e = cudaSuccess;
+  if (!plan_swarm(c, (int64_t)B, pl, e)) {
+    psso_destroy(c);
+    return e != cudaSuccess ? cuda_fail(nullptr, e, "psso_solve_batch plan")
+                            : fail(nullptr, PSSO_E_UNSUPPORTED, "no whole-run kernel for this batch");
+  }
+  const int G = pl.G;
+  struct Buf { void* p = nullptr; } X, P, pf, gb, gf, tr, ep, sf, si, sn, sr, sd, bad;
   cudaStream_t s = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   auto cleanup = [&]() {
-    for (Buf* b : {&X, &P, &pf, &gb, &gf, &tr, &bar, &sf, &si, &sr, &sd, &bad}) cudaFree(b->p);
+    for (Buf* b : {&X, &P, &pf, &gb, &gf, &tr, &ep, &sf, &si, &sn, &sr, &sd, &bad}) cudaFree(b->p);
     if (e0) cudaEventDestroy(e0);
     if (e1) cudaEventDestroy(e1);
     if (s) cudaStreamDestroy(s);
@@ -1184,9 +1241,10 @@ int psso_solve_batch(const psso_config* cfg, const uint64_t* seeds, int32_t nsee
       (e = cudaMalloc(&gb.p, B * D * es)) != cudaSuccess ||
       (e = cudaMalloc(&gf.p, B * 8)) != cudaSuccess ||
       (e = cudaMalloc(&tr.p, B * (size_t)niter * 8)) != cudaSuccess ||
-      (e = cudaMalloc(&bar.p, B * sizeof(unsigned int))) != cudaSuccess ||
+      (e = cudaMalloc(&ep.p, B * 2 * G * sizeof(unsigned int))) != cudaSuccess ||
       (e = cudaMalloc(&sf.p, B * 2 * G * 8)) != cudaSuccess ||
       (e = cudaMalloc(&si.p, B * 2 * G * 8)) != cudaSuccess ||
+      (e = cudaMalloc(&sn.p, B * 2 * G * 4)) != cudaSuccess ||
       (e = cudaMalloc(&sr.p, B * 2 * G * D * es)) != cudaSuccess ||
       (e = cudaMalloc(&sd.p, B * 8)) != cudaSuccess ||
       (e = cudaMalloc(&bad.p, B * 8)) != cudaSuccess ||
@@ -1202,15 +1260,18 @@ int psso_solve_batch(const psso_config* cfg, const uint64_t* seeds, int32_t nsee
   c->stream = s;
   c->bound = true;
   TileParams p = tile_params(c, fused_mode(c), 0, nullptr, true);
-  p.off_bar = c->swarm_off_bar;
-  p.off_scr = c->swarm_off_scr;
+  p.off_bar = pl.off_bar;
+  p.off_scr = pl.off_scr;
+  p.off_xs = pl.off_xs;
   SwarmParams sp;
   std::memset(&sp, 0, sizeof sp);
   sp.rows = (int64_t)N;
   sp.G = G;
-  sp.bar = (unsigned int*)bar.p;
+  sp.gpc = pl.gpc;
+  sp.epoch = (unsigned int*)ep.p;
   sp.slot_f = (double*)sf.p;
   sp.slot_i = (int64_t*)si.p;
+  sp.slot_new = (int32_t*)sn.p;
   sp.slot_row = sr.p;
   sp.traj = (double*)tr.p;
   sp.traj_stride = niter;
@@ -1219,11 +1280,11 @@ int psso_solve_batch(const psso_config* cfg, const uint64_t* seeds, int32_t nsee
   sp.seeds = (const uint64_t*)sd.p;
   sp.bad = (unsigned long long*)bad.p;
   auto launch = [&]() -> cudaError_t {
-    cudaError_t r = cudaMemsetAsync(bar.p, 0, B * sizeof(unsigned int), s);
+    cudaError_t r = cudaMemsetAsync(ep.p, 0, B * 2 * G * sizeof(unsigned int), s);
     if (r != cudaSuccess) return r;
     void* args[] = {(void*)&p, (void*)&sp};
-    if (G > 1) return cudaLaunchCooperativeKernel(c->swarm_fn, dim3(G, (unsigned)B), dim3(NT), args, c->swarm_smem, s);
-    return cudaLaunchKernel(c->swarm_fn, dim3(1, (unsigned)B), dim3(NT), args, c->swarm_smem, s);
+    if (G > 1) return cudaLaunchCooperativeKernel(pl.fn, dim3(G, (unsigned)B), dim3(NT), args, pl.smem, s);
+    return cudaLaunchKernel(pl.fn, dim3(1, (unsigned)B), dim3(NT), args, pl.smem, s);
   };
   sp.do_init = 1;  // initialize (core.py:196-210), outside the timed loop (parallel.py:190)
   sp.niter = 0;

@@ -985,6 +985,14 @@ __device__ __forceinline__ T chain_term1(T x, T nb, int e) {
 template <typename T, int M>
 __host__ __device__ constexpr int chain_row_stride() { return 8 * M * (int)sizeof(T); }
 
+// Row store of the chain step: streaming global store, or a plain store when
+// the swarm is resident in shared memory (RES, k_swarm).
+template <typename T, bool RES>
+__device__ __forceinline__ void st_row(T* p, T v) {
+  if constexpr (RES) *p = v;
+  else stg_stream<T, 1>(p, VecT<T, 1>{{v}});
+}
+
 // Per-launch constants of the chain step (per swarm in the batched kernel).
 struct ChainEnv {
   void* X;                // rows x D positions / pbests of this swarm (shard)
@@ -1003,11 +1011,11 @@ struct ChainEnv {
 // x holds the loaded positions, pv the pbests unless INIT).  Positions, X
 // store, fitness in numpy order, pbest/p_f/sol_f bookkeeping and the
 // lexicographic candidate.  The whole warp must call it (shuffles).
-template <typename T, int FN, int RNG, int M, bool INIT, bool FULL>
+template <typename T, int FN, int RNG, int M, bool INIT, bool FULL, bool RES = false>
 __device__ __forceinline__ void chain_step(const TileParams& p, const ChainEnv& ev, const T* gb,
                                            const uint64_t* xg, T* scr, int64_t r, bool rv,
                                            T (&x)[M], const T (&pv)[M], double pf_row,
-                                           double& best_f, int64_t& best_i) {
+                                           double& best_f, int64_t& best_i, int& best_new) {
   using N = Num<T>;
   const int lane = threadIdx.x & 31, k = lane & 7, seg = lane & ~7;
   const int D = ev.D;
@@ -1036,9 +1044,9 @@ __device__ __forceinline__ void chain_step(const TileParams& p, const ChainEnv& 
           h = ((uint64_t)w.w[s2] << 32) | w.w[s2 + 1];
         }
         const T v = (T)__dadd_rn(p.var_min, __dmul_rn(p.span, unit53(h)));
-        stg_stream<T, 1>(pr + j, VecT<T, 1>{{v}});
+        st_row<T, RES>(pr + j, v);
         x[m] = v;
-        stg_stream<T, 1>(xr + j, VecT<T, 1>{{v}});
+        st_row<T, RES>(xr + j, v);
       } else {
         x[m] = (T)0;
       }
@@ -1071,7 +1079,7 @@ __device__ __forceinline__ void chain_step(const TileParams& p, const ChainEnv& 
         v = search_chunk<T, 1, 1>(p, xv, pb, gv, 0, 0, j, (uint64_t)gi, ev.t, ev.seed).v[0];
       }
       x[m] = v;
-      if (rv && (FULL || j < D)) stg_stream<T, 1>(xr + j, VecT<T, 1>{{v}});
+      if (rv && (FULL || j < D)) st_row<T, RES>(xr + j, v);
     }
   }
 
@@ -1158,21 +1166,27 @@ __device__ __forceinline__ void chain_step(const TileParams& p, const ChainEnv& 
       if (ev.sol_f && ((mode & M_SOLF) || !isfinite(f))) ev.sol_f[r] = f;
     }
     double pf = f;
+    bool fresh_row = INIT;  // the row's pbest was (re)written now
     if (INIT) {
       if (k == 0) ev.p_f[r] = f;
     } else {
       const bool imp = f <= pf_row;  // parallel.py:109, ties refresh
       pf = imp ? f : pf_row;
+      fresh_row = imp;
       if (imp) {
         if (k == 0) ev.p_f[r] = f;
 #pragma unroll
         for (int m = 0; m < M; ++m) {
           const int j = k + 8 * m;
-          if (FULL || j < D) stg_stream<T, 1>(pr + j, VecT<T, 1>{{x[m]}});
+          if (FULL || j < D) st_row<T, RES>(pr + j, x[m]);
         }
       }
     }
-    if (k == 0 && lex_less(pf, gi, best_f, best_i)) { best_f = pf; best_i = gi; }
+    if (k == 0 && lex_less(pf, gi, best_f, best_i)) {
+      best_f = pf;
+      best_i = gi;
+      best_new = fresh_row;
+    }
   }
 }
 
@@ -1325,7 +1339,9 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, PSSO_CHAIN_MINB)
 #pragma unroll
       for (int m = 0; m < M; ++m) pv[m] = (T)0;
     }
-    chain_step<T, FN, RNG, M, INIT, FULL>(p, ev, gb, xg, scr, r, rv, x, pv, pf_row, best_f, best_i);
+    int best_new = 0;
+    chain_step<T, FN, RNG, M, INIT, FULL>(p, ev, gb, xg, scr, r, rv, x, pv, pf_row, best_f, best_i,
+                                          best_new);
   }
   cta_candidate<NW>(best_f, best_i, red_f, red_i, p.slot_f + blockIdx.x, p.slot_i + blockIdx.x);
 }

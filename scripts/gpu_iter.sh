@@ -13,7 +13,7 @@ for w in ${WORKLOADS:-c3 c3f32 c4 c5 c3sphere}; do
 import json
 for l in open('gpurun_out/bench_$w.log'):
   if l.startswith('{'):
-    d=json.loads(l); r=d['roofline']; print('$w', '%.4g pvu/s'%d['value'], 'ms/step %.4f'%d['ms_per_step'], 'kernel %.4f ms'%r['kernel_ms'], 'frac %.3f'%r['frac'], 'e2e %.4g'%d['e2e']['value'])
+    d=json.loads(l); r=d['roofline']; print('$w', '%.4g pvu/s'%d['value'], 'ms/step %.4f'%d['ms_per_step'], 'kernel %.4f ms'%r['kernel_ms_per_iteration'], 'frac %.3f'%r['frac'], 'e2e %.4g'%d['e2e']['value'])
 " || tail -5 gpurun_out/bench_$w.log
 done
 if [ -n "$NCU" ]; then

@@ -1,6 +1,7 @@
 #!/bin/bash
 # One full GPU pass: smoke, gpu tests, the contract bench (+ reference arm), the
-# other BASELINE workloads, the ncu launch list and one full capture of the top kernel.
+# other BASELINE workloads, the ncu launch list and full captures (steady state,
+# iteration ~250) of the iteration kernel of the main workloads.
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > gpurun_out/nvsmi.txt 2>&1
@@ -8,23 +9,18 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 tail -2 gpurun_out/smoke.log
 if [ -z "$SKIP_TESTS" ]; then
 timeout 1200 python -m pytest tests -m gpu -q --timeout 600 --durations=15 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-tail -25 gpurun_out/pytest_gpu.log
+tail -3 gpurun_out/pytest_gpu.log
 fi
 timeout 600 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
 tail -2 gpurun_out/bench.log
 timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref.log 2>&1; tail -1 gpurun_out/bench_ref.log
-for w in ${WORKLOADS:-c3f32 c4 c5 c2 c3sphere}; do
-  timeout 400 python bench.py --steps 50 --warmup 5 --no-cpu --workload $w > gpurun_out/bench_$w.log 2>&1
+for w in ${WORKLOADS:-c3f32 c4 c5 c2 c2f4 c2f6 c2f7 c1 c3sphere}; do
+  timeout 400 python bench.py --steps ${STEPS:-200} --warmup 5 --no-cpu --workload $w > gpurun_out/bench_$w.log 2>&1
   python -c "
 import json
 for l in open('gpurun_out/bench_$w.log'):
   if l.startswith('{'):
-    d=json.loads(l); r=d['roofline']; print('$w', '%.4g pvu/s'%d['value'], 'ms/step %.4f'%d['ms_per_step'], 'kernel %.4f ms'%r['kernel_ms'], 'frac %.3f'%r['frac'], 'e2e %.4g'%d['e2e']['value'])
+    d=json.loads(l); r=d['roofline']; print('$w', '%.4g pvu/s'%d['value'], 'ms/step %.4f'%d['ms_per_step'], 'kernel %.4f ms'%r['kernel_ms_per_iteration'], 'frac %.3f'%r['frac'], 'e2e %.4g'%d['e2e']['value'], r['kernel'])
 " || tail -5 gpurun_out/bench_$w.log
 done
-if [ -z "$SKIP_NCU" ]; then
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches_c3.csv python bench.py --steps 20 --warmup 3 --no-cpu > gpurun_out/ncu_launch.log 2>&1
-tail -1 gpurun_out/ncu_launch.log
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:${NCU_KERNEL:-k_chain} -s 5 -c 1 -o gpurun_out/prof_c3 python bench.py --steps 5 --warmup 3 --no-cpu > gpurun_out/ncu_c3.log 2>&1
-tail -2 gpurun_out/ncu_c3.log
-fi
+if [ -z "$SKIP_NCU" ]; then LAUNCHES=1 bash scripts/gpu_ncu.sh; fi

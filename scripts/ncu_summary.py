@@ -3,6 +3,7 @@
 
     python scripts/ncu_summary.py report  prof.ncu-rep [--units N] > profiles/x.txt
     python scripts/ncu_summary.py launches launches.csv            > profiles/y.txt
+    python scripts/ncu_summary.py traffic prof.ncu-rep --workload c3 --bench-log b.log
 
 `report`: one `ncu --set full` capture -> duration, DRAM bytes and
 throughput, issue/occupancy, pipe utilisation, warp-stall samples and the
@@ -109,14 +110,41 @@ def launches(path):
         print(f"{k[:70]:70s} {len(v):8d} {sum(v) / len(v):10.2f} {100 * sum(v) / total:6.1f}%")
 
 
+def traffic(path, workload, bench_log):
+    """Record the capture's DRAM bytes per launch in bench_traffic.json for bench.py."""
+    import json
+    import pathlib
+
+    raw = ncu_csv([path, "--page", "raw"])
+    d = dict(zip(raw[0], zip(raw[1], raw[2])))
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    tb = sum(float(d[k][1].replace(",", "")) * scale.get(d[k][0], 1)
+             for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+    kernel = None
+    for line in open(bench_log):
+        if line.startswith("{"):
+            kernel = json.loads(line)["roofline"]["kernel"]
+    out = pathlib.Path(__file__).resolve().parent.parent / "bench_traffic.json"
+    db = json.loads(out.read_text()) if out.exists() else {}
+    db[workload] = {"kernel": kernel, "dram_bytes_per_launch": tb,
+                    "source": f"ncu --set full capture {pathlib.Path(path).name} "
+                              f"({d.get('Kernel Name', ('', '?'))[1]})"}
+    out.write_text(json.dumps(db, indent=1, sort_keys=True) + "\n")
+    print(f"{workload}: {kernel} {tb / 1e9:.4f} GB per launch -> {out.name}")
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("mode", choices=["report", "launches"])
+    ap.add_argument("mode", choices=["report", "launches", "traffic"])
     ap.add_argument("path")
     ap.add_argument("--units", type=int, default=0, help="work units (pvu) in the captured launch")
+    ap.add_argument("--workload", default="c3")
+    ap.add_argument("--bench-log", default=None)
     a = ap.parse_args()
     if a.mode == "report":
         report(a.path, a.units)
+    elif a.mode == "traffic":
+        traffic(a.path, a.workload, a.bench_log)
     else:
         launches(a.path)
 
