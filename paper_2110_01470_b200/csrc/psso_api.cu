@@ -29,6 +29,15 @@ constexpr int GRAPH_CHUNK = 16;  // iterations per captured graph
 #define PSSO_SWARM_MAX_ELEMS (1 << 22)  // N*D up to which psso_run uses the whole-run kernel
 #endif
 
+// Launch plan of the whole-run kernel (k_swarm); see plan_swarm.
+struct SwarmPlan {
+  const void* fn = nullptr;
+  int G = 0, gpc = 0;
+  bool res = false, cl = false;
+  size_t smem = 0;
+  int off_bar = 0, off_scr = 0, off_pub = 0, off_xs = 0;
+};
+
 struct Layout {
   int V, R, G, S, NL;
   bool pre;
@@ -364,11 +373,8 @@ struct psso_ctx {
   size_t ev_used;
   int64_t prof_iters;    // iterations covered by the timed launches
   // whole-run kernel for small swarms (psso_swarm.cuh); null: streaming path
-  const void* swarm_fn;
-  int swarm_G, swarm_gpc;
-  bool swarm_res;
-  size_t swarm_smem;
-  int swarm_off_bar, swarm_off_scr, swarm_off_xs;
+  const void* swarm_fn;   // == swarm.fn
+  SwarmPlan swarm;
   unsigned int* sw_epoch;
   double* sw_slot_f;
   int64_t* sw_slot_i;
@@ -539,38 +545,73 @@ int fused_step(psso_ctx* c, int64_t t, int64_t* t_dev) {
 // RES (rows in smem, gpc row groups per CTA) when the tiles fit and the
 // B x G CTAs can be co-resident; else rows in HBM, one row group per warp.
 // G = 1 needs no co-residency (the swarm barrier is __syncthreads).
-struct SwarmPlan {
-  const void* fn = nullptr;
-  int G = 0, gpc = 0;
-  bool res = false;
-  size_t smem = 0;
-  int off_bar = 0, off_scr = 0, off_xs = 0;
-};
-
+// Launch plan of the whole-run kernel for B swarms of this configuration.
+// Preferred: CL -- one thread-block cluster of G <= 16 CTAs per swarm, rows
+// resident in smem, exchange over DSMEM (clusters are independent, so any
+// number of swarms).  Else the global-memory exchange: RES when the tiles fit
+// and the B x G CTAs can be co-resident; else rows in HBM.  G = 1 needs no
+// co-residency.
 bool plan_swarm(psso_ctx* c, int64_t B, SwarmPlan& sp, cudaError_t& e) {
   const psso_config* cfg = &c->cfg;
   const int64_t rows = cfg->row_hi - cfg->row_lo, D = cfg->nvar;
   const int M = D <= 32 ? 4 : D <= 64 ? 8 : 16;
   const int es = cfg->dtype == PSSO_F64 ? 8 : 4;
-  const int nw = NT / 32;
+  const int nw = PSSO_SWARM_NT / 32;
   const bool smem_fn = cfg->fn_id == 3 || cfg->fn_id == 7 || cfg->fn_id == 8;
   const int64_t ngroups = (rows + 3) / 4;
-  sp.off_bar = (int)align16((size_t)c->LF.off_red + 128 + 64 * M);
-  sp.off_scr = (int)align16((size_t)sp.off_bar + 64);
-  sp.off_xs = (int)align16((size_t)sp.off_scr + (smem_fn ? (size_t)nw * 4 * (8 * M) * es : 0));
+  sp.off_bar = (int)align16((size_t)c->LF.off_red + 16 * nw + 64 * M);
+  sp.off_scr = (int)align16((size_t)sp.off_bar + 24 + 4 * (nw + 1));
+  sp.off_pub = (int)align16((size_t)sp.off_scr + (smem_fn ? (size_t)nw * 4 * (8 * M) * es : 0));
+  sp.off_xs = (int)align16((size_t)sp.off_pub + 64 + 2 * (size_t)D * es);
   e = cudaSuccess;
+  auto res_smem = [&](int64_t gpc) { return (size_t)sp.off_xs + (size_t)gpc * 4 * (D * 2 * es + 8); };
+  const char* nc = std::getenv("PSSO_SWARM_NO_CLUSTER");
+  if (!(nc && *nc && *nc != '0')) {
+    const char* gs = std::getenv("PSSO_SWARM_G");
+    // about half the warps of each CTA busy: shorter per-CTA chains beat fewer CTAs
+    int64_t G = std::max<int64_t>(1, std::min<int64_t>(16, (ngroups + 7) / 8));
+    if (gs && *gs) G = std::max<int64_t>(1, std::min<int64_t>(16, std::atoll(gs)));
+    const int64_t gpc = (ngroups + G - 1) / G;
+    G = (ngroups + gpc - 1) / gpc;
+    const size_t smem = res_smem(gpc);
+    const void* f = swarm_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, M, true, true);
+    if (f && smem <= 227 * 1024) {
+      if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess ||
+          (G > 8 && (e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess))
+        return false;
+      cudaLaunchConfig_t lc = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = (unsigned)G;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      lc.gridDim = dim3((unsigned)G, 1, 1);
+      lc.blockDim = dim3(PSSO_SWARM_NT, 1, 1);
+      lc.dynamicSmemBytes = smem;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      int nclusters = 0;
+      if ((e = cudaOccupancyMaxActiveClusters(&nclusters, f, &lc)) != cudaSuccess) {
+        e = cudaSuccess;  // cluster size not schedulable: fall through
+        cudaGetLastError();
+      } else if (nclusters >= 1) {
+        sp.fn = f; sp.G = (int)G; sp.gpc = (int)gpc; sp.res = true; sp.cl = true; sp.smem = smem;
+        return true;
+      }
+    }
+  }
   auto try_plan = [&](bool res, int64_t gpc, int64_t G) -> bool {
-    const size_t smem = res ? (size_t)sp.off_xs + (size_t)gpc * 4 * (D * 2 * es + 8) : (size_t)sp.off_xs;
+    const size_t smem = res ? res_smem(gpc) : (size_t)sp.off_xs;
     if (smem > 227 * 1024) return false;
-    const void* f = swarm_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, M, res);
+    const void* f = swarm_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, M, res, false);
     if (!f) return false;
     int per_sm = 0;
     if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess ||
-        (e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, NT, smem)) != cudaSuccess)
+        (e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, PSSO_SWARM_NT, smem)) != cudaSuccess)
       return false;
     const int64_t cap = (int64_t)per_sm * c->num_sms;
     if (per_sm < 1 || (G > 1 && G * B > cap)) return false;
-    sp.fn = f; sp.G = (int)G; sp.gpc = (int)gpc; sp.res = res; sp.smem = smem;
+    sp.fn = f; sp.G = (int)G; sp.gpc = (int)gpc; sp.res = res; sp.cl = false; sp.smem = smem;
     return true;
   };
   const char* g = std::getenv("PSSO_SWARM_GPC");
@@ -580,16 +621,38 @@ bool plan_swarm(psso_ctx* c, int64_t B, SwarmPlan& sp, cudaError_t& e) {
   if (try_plan(true, ngroups, 1)) return true;                       // resident, one CTA per swarm
   if (e != cudaSuccess) return false;
   int per_sm = 0;                                                     // rows in HBM
-  const void* f = swarm_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, M, false);
+  const void* f = swarm_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, M, false, false);
   if (!f) return false;
   if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.off_xs)) != cudaSuccess ||
-      (e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, NT, sp.off_xs)) != cudaSuccess || per_sm < 1)
+      (e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, PSSO_SWARM_NT, sp.off_xs)) != cudaSuccess || per_sm < 1)
     return false;
   const int64_t cap = (int64_t)per_sm * c->num_sms;
   int64_t G = std::max<int64_t>(1, std::min<int64_t>((ngroups + nw - 1) / nw, cap / B));
   if (G * B > cap) G = 1;
-  sp.fn = f; sp.G = (int)G; sp.gpc = nw; sp.res = false; sp.smem = sp.off_xs;
+  sp.fn = f; sp.G = (int)G; sp.gpc = nw; sp.res = false; sp.cl = false; sp.smem = sp.off_xs;
   return true;
+}
+
+// Launch B swarms of the plan (grid G x B; clusters of G, or cooperative).
+cudaError_t launch_swarm(const SwarmPlan& pl, int64_t B, void** args, cudaStream_t s) {
+  if (pl.cl) {
+    cudaLaunchConfig_t lc = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)pl.G;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.gridDim = dim3((unsigned)pl.G, (unsigned)B, 1);
+    lc.blockDim = dim3(PSSO_SWARM_NT, 1, 1);
+    lc.dynamicSmemBytes = pl.smem;
+    lc.stream = s;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    return cudaLaunchKernelExC(&lc, pl.fn, args);
+  }
+  if (pl.G > 1)  // co-residency of the swarm's CTAs is required by its barrier
+    return cudaLaunchCooperativeKernel(pl.fn, dim3(pl.G, (unsigned)B), dim3(PSSO_SWARM_NT), args, pl.smem, s);
+  return cudaLaunchKernel(pl.fn, dim3(1, (unsigned)B), dim3(PSSO_SWARM_NT), args, pl.smem, s);
 }
 
 }  // namespace
@@ -732,7 +795,6 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
     c->fused_grid = (int)std::min<int64_t>((rows + rpc - 1) / rpc, (int64_t)per_sm_fused * c->num_sms);
   }
   c->swarm_fn = nullptr;
-  c->swarm_G = 0;
   if (c->chain && cfg->row_lo == 0 && cfg->row_hi == cfg->nsol &&
       rows * cfg->nvar <= PSSO_SWARM_MAX_ELEMS) {  // small swarm: the whole run in one launch
     const char* off = std::getenv("PSSO_NO_SWARM");
@@ -744,13 +806,7 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
       }
       if (sp.fn) {
         c->swarm_fn = sp.fn;
-        c->swarm_G = sp.G;
-        c->swarm_gpc = sp.gpc;
-        c->swarm_res = sp.res;
-        c->swarm_smem = sp.smem;
-        c->swarm_off_bar = sp.off_bar;
-        c->swarm_off_scr = sp.off_scr;
-        c->swarm_off_xs = sp.off_xs;
+        c->swarm = sp;
       }
     }
   }
@@ -762,7 +818,7 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
     char b[160];
     if (c->swarm_fn)
       std::snprintf(b, sizeof b, "k_swarm<%s,f%d,%s,M=%d%s> x%d CTAs", tn, cfg->fn_id, rn, M,
-                    c->swarm_res ? ",smem-resident" : "", c->swarm_G);
+                    c->swarm.cl ? ",cluster" : c->swarm.res ? ",smem-resident" : "", c->swarm.G);
     else if (c->rows_w)
       std::snprintf(b, sizeof b, "k_rows<%s,f%d,%s,W=%d>", tn, cfg->fn_id, rn, c->rows_w);
     else if (c->chain)
@@ -786,7 +842,7 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
   }
   if (c->swarm_fn) {
     const size_t es = cfg->dtype == PSSO_F64 ? 8 : 4;
-    const size_t G = (size_t)c->swarm_G;
+    const size_t G = (size_t)c->swarm.G;
     const uint64_t seed = cfg->seed;
     if ((e = cudaMalloc(&c->sw_epoch, 2 * G * sizeof(unsigned int))) != cudaSuccess ||
         (e = cudaMalloc(&c->sw_slot_f, 2 * G * sizeof(double))) != cudaSuccess ||
@@ -876,16 +932,17 @@ int psso_step(psso_ctx* c, int64_t t) {
 // the whole loop as one k_swarm launch (small swarms)
 static int swarm_run(psso_ctx* c, int64_t t0, int64_t niter) {
   TileParams p = tile_params(c, fused_mode(c), t0, nullptr, true);
-  p.off_bar = c->swarm_off_bar;
-  p.off_scr = c->swarm_off_scr;
-  p.off_xs = c->swarm_off_xs;
+  p.off_bar = c->swarm.off_bar;
+  p.off_scr = c->swarm.off_scr;
+  p.off_leaf = c->swarm.off_pub;
+  p.off_xs = c->swarm.off_xs;
   SwarmParams sp;
   std::memset(&sp, 0, sizeof sp);
   sp.t0 = t0;
   sp.niter = niter;
   sp.rows = c->cfg.row_hi - c->cfg.row_lo;
-  sp.G = c->swarm_G;
-  sp.gpc = c->swarm_gpc;
+  sp.G = c->swarm.G;
+  sp.gpc = c->swarm.gpc;
   sp.do_init = 0;
   sp.epoch = c->sw_epoch;
   sp.slot_f = c->sw_slot_f;
@@ -899,7 +956,7 @@ static int swarm_run(psso_ctx* c, int64_t t0, int64_t niter) {
   sp.seeds = c->sw_seed;
   sp.sol_f = c->buf.sol_f;
   sp.bad = c->bad;
-  CK(c, cudaMemsetAsync(c->sw_epoch, 0, 2 * (size_t)c->swarm_G * sizeof(unsigned int), c->stream));
+  CK(c, cudaMemsetAsync(c->sw_epoch, 0, 2 * (size_t)c->swarm.G * sizeof(unsigned int), c->stream));
   const bool timed = c->profiling;
   if (timed) {
     if (c->ev_used + 2 > c->ev.size()) {
@@ -911,12 +968,30 @@ static int swarm_run(psso_ctx* c, int64_t t0, int64_t niter) {
     }
     CK(c, cudaEventRecord(c->ev[c->ev_used], c->stream));
   }
+#if PSSO_SWARM_TRACE
+  unsigned long long* trace = nullptr;
+  CK(c, cudaMalloc(&trace, (size_t)niter * 4 * sizeof(unsigned long long)));
+  sp.trace = trace;
+#endif
   void* args[] = {(void*)&p, (void*)&sp};
-  if (c->swarm_G > 1)  // co-residency of the swarm's CTAs is required by its barrier
-    CK(c, cudaLaunchCooperativeKernel(c->swarm_fn, dim3(c->swarm_G, 1), dim3(NT), args, c->swarm_smem, c->stream));
-  else
-    CK(c, cudaLaunchKernel(c->swarm_fn, dim3(1, 1), dim3(NT), args, c->swarm_smem, c->stream));
+  CK(c, launch_swarm(c->swarm, 1, args, c->stream));
   c->launches++;
+#if PSSO_SWARM_TRACE
+  {  // phase breakdown of CTA 0 (diagnostic builds only)
+    std::vector<unsigned long long> h((size_t)niter * 4);
+    CK(c, cudaStreamSynchronize(c->stream));
+    CK(c, cudaMemcpy(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost));
+    cudaFree(trace);
+    double ph[3] = {0, 0, 0}, tot = 0;
+    for (int64_t i = 0; i < niter; ++i) {
+      for (int k = 0; k < 3; ++k) ph[k] += (double)(h[i * 4 + k + 1] - h[i * 4 + k]);
+      tot += (double)(h[i * 4 + 3] - h[i * 4]);
+    }
+    std::fprintf(stderr, "[swarm trace] G=%d niter=%lld per iteration (ns): compute+publish %.0f  wait %.0f  "
+                 "take+sync %.0f  total %.0f\n", c->swarm.G, (long long)niter, ph[0] / niter, ph[1] / niter,
+                 ph[2] / niter, tot / niter);
+  }
+#endif
   if (timed) {
     CK(c, cudaEventRecord(c->ev[c->ev_used + 1], c->stream));
     c->ev_used += 2;
@@ -1262,6 +1337,7 @@ int psso_solve_batch(const psso_config* cfg, const uint64_t* seeds, int32_t nsee
   TileParams p = tile_params(c, fused_mode(c), 0, nullptr, true);
   p.off_bar = pl.off_bar;
   p.off_scr = pl.off_scr;
+  p.off_leaf = pl.off_pub;
   p.off_xs = pl.off_xs;
   SwarmParams sp;
   std::memset(&sp, 0, sizeof sp);
@@ -1283,8 +1359,7 @@ int psso_solve_batch(const psso_config* cfg, const uint64_t* seeds, int32_t nsee
     cudaError_t r = cudaMemsetAsync(ep.p, 0, B * 2 * G * sizeof(unsigned int), s);
     if (r != cudaSuccess) return r;
     void* args[] = {(void*)&p, (void*)&sp};
-    if (G > 1) return cudaLaunchCooperativeKernel(pl.fn, dim3(G, (unsigned)B), dim3(NT), args, pl.smem, s);
-    return cudaLaunchKernel(pl.fn, dim3(1, (unsigned)B), dim3(NT), args, pl.smem, s);
+    return launch_swarm(pl, (int64_t)B, args, s);
   };
   sp.do_init = 1;  // initialize (core.py:196-210), outside the timed loop (parallel.py:190)
   sp.niter = 0;

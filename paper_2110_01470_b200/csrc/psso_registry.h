@@ -23,14 +23,14 @@ inline const void* rows_kernel(int dtype, int rng, int fn, int w) {
   return rng == 0 ? rows_kernel_f32_ref(fn, w) : rows_kernel_f32_philox(fn, w);
 }
 
-const void* swarm_kernel_f64_ref(int fn, int m, bool res);
-const void* swarm_kernel_f64_philox(int fn, int m, bool res);
-const void* swarm_kernel_f32_ref(int fn, int m, bool res);
-const void* swarm_kernel_f32_philox(int fn, int m, bool res);
+const void* swarm_kernel_f64_ref(int fn, int m, bool res, bool cl);
+const void* swarm_kernel_f64_philox(int fn, int m, bool res, bool cl);
+const void* swarm_kernel_f32_ref(int fn, int m, bool res, bool cl);
+const void* swarm_kernel_f32_philox(int fn, int m, bool res, bool cl);
 
-inline const void* swarm_kernel(int dtype, int rng, int fn, int m, bool res) {
-  if (dtype == 0) return rng == 0 ? swarm_kernel_f64_ref(fn, m, res) : swarm_kernel_f64_philox(fn, m, res);
-  return rng == 0 ? swarm_kernel_f32_ref(fn, m, res) : swarm_kernel_f32_philox(fn, m, res);
+inline const void* swarm_kernel(int dtype, int rng, int fn, int m, bool res, bool cl) {
+  if (dtype == 0) return rng == 0 ? swarm_kernel_f64_ref(fn, m, res, cl) : swarm_kernel_f64_philox(fn, m, res, cl);
+  return rng == 0 ? swarm_kernel_f32_ref(fn, m, res, cl) : swarm_kernel_f32_philox(fn, m, res, cl);
 }
 
 inline const void* chain_kernel(int dtype, int rng, int fn, int m, bool init, bool full) {

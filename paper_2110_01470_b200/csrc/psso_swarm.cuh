@@ -26,9 +26,15 @@
 // numpy-order fitness as the streaming path: results are bit-identical to it.
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "psso_device.cuh"
 
 namespace psso {
+
+#ifndef PSSO_SWARM_NT
+#define PSSO_SWARM_NT 512  // 16 warps: four per scheduler to hide the chain latency
+#endif
 
 struct SwarmParams {
   int64_t t0, niter;
@@ -49,7 +55,22 @@ struct SwarmParams {
   const uint64_t* seeds;    // [B]
   double* sol_f;            // [B][rows] or null
   unsigned long long* bad;  // [B]
+  unsigned long long* trace;  // PSSO_SWARM_TRACE builds: [niter][4] phase timestamps of CTA 0
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#ifndef PSSO_SWARM_TRACE
+#define PSSO_SWARM_TRACE 0
+#endif
+#define PSSO_TRACE(it, k)                                                            \
+  do {                                                                               \
+    if (PSSO_SWARM_TRACE && sp.trace && c == 0 && b == 0 && tid == 0 && (it) >= 0)   \
+      sp.trace[(it) * 4 + (k)] = gtimer();                                           \
+  } while (0)
 
 __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
   unsigned int v;
@@ -60,16 +81,22 @@ __device__ __forceinline__ void st_release_u32(unsigned int* p, unsigned int v) 
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// CL (G <= 16 CTAs form one thread-block cluster): each CTA publishes its
+// candidate record and row in its OWN shared memory, one hardware cluster
+// barrier (barrier.cluster arrive.release / wait.acquire) replaces the
+// epoch tags, and the records and the winner row are read over DSMEM.
+//
 // Shared memory (offsets in TileParams, host: swarm layout in psso_create):
 //   0        gbest (D of T)
 //   off_red  warp reduction (16 * NW) + xs30(gamma*(j+1)) table (8 * 8M)
-//   off_bar  winner record (f, i, slot, new) + per-warp "new" flags + stop
+//   off_bar  winner record (f, i, slot, new: 24 B) + per-warp "new" flags + stop
 //   off_scr  per-warp smem rows [4][8M] (f3, f7, f8)
+//   off_leaf CL: published records [2][f, i, new|bad] + rows [2][D]
 //   off_xs   RES: X rows [4 gpc][D], P rows [4 gpc][D], p_f [4 gpc]
-template <typename T, int FN, int RNG, int M, bool RES>
-__global__ void __launch_bounds__(PSSO_CHAIN_NT, 1)
+template <typename T, int FN, int RNG, int M, bool RES, bool CL>
+__global__ void __launch_bounds__(PSSO_SWARM_NT, 1)
     k_swarm(const __grid_constant__ TileParams p, const __grid_constant__ SwarmParams sp) {
-  constexpr int NTC = PSSO_CHAIN_NT;
+  constexpr int NTC = PSSO_SWARM_NT;
   constexpr int NW = NTC / 32;
   extern __shared__ __align__(128) unsigned char smem[];
   T* gb = reinterpret_cast<T*>(smem);
@@ -81,6 +108,13 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, 1)
   int* win_c = reinterpret_cast<int*>(smem + p.off_bar + 16);
   int* win_n = reinterpret_cast<int*>(smem + p.off_bar + 20);
   int* red_n = reinterpret_cast<int*>(smem + p.off_bar + 24);
+
+  double* pub_f = reinterpret_cast<double*>(smem + p.off_leaf);       // CL: [2]
+  int64_t* pub_i = reinterpret_cast<int64_t*>(smem + p.off_leaf + 16);
+  int* pub_n = reinterpret_cast<int*>(smem + p.off_leaf + 32);
+  T* pub_row = reinterpret_cast<T*>(smem + p.off_leaf + 64);          // CL: [2][D]
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = lane & 7;
@@ -145,6 +179,7 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, 1)
   // the epoch's records is the same in every CTA, so all stop together
   // (a direct read of the flag could differ between CTAs and deadlock).
   // Returns that stop decision.  t < 0: no trajectory entry.
+  int64_t trace_it = -1;
   auto exchange = [&](double best_f, int64_t best_i, int best_new, bool is_init, int64_t t) -> bool {
     ++epoch;
     const int par = (int)(epoch & 1);
@@ -163,10 +198,67 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, 1)
           best_f = red_f[w]; best_i = red_i[w]; best_new = red_n[w];
         }
       const int seen_bad = *(volatile unsigned long long*)ev.bad != ~0ull;
-      sf[par * G + c] = best_f;
-      si[par * G + c] = best_i;
-      sn[par * G + c] = (best_new & 1) | (seen_bad << 1);
+      if constexpr (CL) {
+        pub_f[par] = best_f;
+        pub_i[par] = best_i;
+        pub_n[par] = (best_new & 1) | (seen_bad << 1);
+      } else {
+        sf[par * G + c] = best_f;
+        si[par * G + c] = best_i;
+        sn[par * G + c] = (best_new & 1) | (seen_bad << 1);
+      }
       red_i[0] = best_i;
+    }
+    if constexpr (CL) {
+      __syncthreads();
+      const int64_t bi = red_i[0];
+      if (bi != INT64_MAX)
+        for (int j = tid; j < D; j += NTC) pub_row[par * D + j] = Pb[(bi - r0) * D + j];
+      PSSO_TRACE(trace_it, 1);
+      cluster.sync();  // every CTA's record and row are published
+      if (warp == 0) {
+        double wf = CUDART_INF;
+        int64_t wi = INT64_MAX;
+        int wc = 0, wn = 0, stop = 0;
+        if (lane < G) {
+          const double* rf = cluster.map_shared_rank(pub_f, lane);
+          const int64_t* ri = cluster.map_shared_rank(pub_i, lane);
+          const int* rn = cluster.map_shared_rank(pub_n, lane);
+          wf = rf[par];
+          wi = ri[par];
+          wn = rn[par];
+          wc = lane;
+          stop = wn >> 1;
+          wn &= 1;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double of = __shfl_xor_sync(0xffffffffu, wf, o);
+          const int64_t oi = __shfl_xor_sync(0xffffffffu, wi, o);
+          const int oc = __shfl_xor_sync(0xffffffffu, wc, o);
+          const int on = __shfl_xor_sync(0xffffffffu, wn, o);
+          stop |= __shfl_xor_sync(0xffffffffu, stop, o);
+          if (lex_less(of, oi, wf, wi)) { wf = of; wi = oi; wc = oc; wn = on; }
+        }
+        if (lane == 0) { *win_f = wf; *win_i = wi; *win_c = wc; *win_n = wn; red_n[NW] = stop; }
+      }
+      PSSO_TRACE(trace_it, 2);
+      __syncthreads();
+      const double wf = *win_f;
+      const int64_t wi = *win_i;
+      const bool take = wi != INT64_MAX && (is_init || wf <= gf);
+      if (take) {
+        if (wi != gi_inc || *win_n) {
+          const T* src = cluster.map_shared_rank(pub_row, *win_c) + par * D;
+          for (int j = tid; j < D; j += NTC) gb[j] = src[j];
+        }
+        gf = wf;
+        gi_inc = wi;
+      }
+      if (t >= 0 && c == 0 && tid == 0 && sp.traj) sp.traj[b * sp.traj_stride + t] = gf;  // :212
+      const bool stop = red_n[NW] != 0;
+      __syncthreads();
+      return stop;
     }
     __syncthreads();
     const int64_t bi = red_i[0];
@@ -177,6 +269,7 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, 1)
       __threadfence();
       st_release_u32(sep + par * G + c, epoch);
     }
+    PSSO_TRACE(trace_it, 1);
     if (warp == 0) {  // wait for the epoch's G records (the swarm barrier) and reduce
       double wf = CUDART_INF;
       int64_t wi = INT64_MAX;
@@ -201,6 +294,7 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, 1)
       if (lane == 0) { *win_f = wf; *win_i = wi; *win_c = wc; *win_n = wn; red_n[NW] = stop; }
       __threadfence();
     }
+    PSSO_TRACE(trace_it, 2);
     __syncthreads();
     const double wf = *win_f;
     const int64_t wi = *win_i;
@@ -251,6 +345,8 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, 1)
   for (int64_t it = 0; it < sp.niter && !stop; ++it) {
     const int64_t t = sp.t0 + it;
     ev.t = t;
+    trace_it = it;
+    PSSO_TRACE(it, 0);
     if constexpr (RNG == 0) {
       ev.rootb = root64(ev.seed, STREAM_BRANCH, (uint64_t)t);
       ev.rootf = root64(ev.seed, STREAM_FRESH, (uint64_t)t);
@@ -276,6 +372,7 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, 1)
                                                    best_f, best_i, best_new);
     }
     stop = exchange(best_f, best_i, best_new, false, t);
+    PSSO_TRACE(it, 3);
   }
 
   if constexpr (RES) {  // the CTA's rows back to HBM
@@ -289,6 +386,7 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, 1)
     for (int j = tid; j < D; j += NTC) gbp[j] = gb[j];
     if (tid == 0) sp.g_f[b] = gf;
   }
+  if constexpr (CL) cluster.sync();  // no CTA leaves while its smem may still be read
 }
 
 }  // namespace psso

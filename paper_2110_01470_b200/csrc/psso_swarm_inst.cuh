@@ -6,14 +6,17 @@
 
 namespace psso {
 
-#define PSSO_SWARM_M(FN, M)                                                             \
-  if (m == M) return res ? (const void*)k_swarm<PSSO_T, FN, PSSO_RNG, M, true>          \
-                         : (const void*)k_swarm<PSSO_T, FN, PSSO_RNG, M, false>;
+#define PSSO_SWARM_M(FN, M)                                                                    \
+  if (m == M) {                                                                                \
+    if (cl) return res ? (const void*)k_swarm<PSSO_T, FN, PSSO_RNG, M, true, true> : nullptr;  \
+    return res ? (const void*)k_swarm<PSSO_T, FN, PSSO_RNG, M, true, false>                    \
+               : (const void*)k_swarm<PSSO_T, FN, PSSO_RNG, M, false, false>;                  \
+  }
 #define PSSO_SWARM(FN) \
   case FN:             \
     PSSO_SWARM_M(FN, 4) PSSO_SWARM_M(FN, 8) PSSO_SWARM_M(FN, 16) return nullptr;
 
-const void* PSSO_NAME(swarm_kernel)(int fn, int m, bool res) {
+const void* PSSO_NAME(swarm_kernel)(int fn, int m, bool res, bool cl) {
   switch (fn) {
     PSSO_SWARM(0) PSSO_SWARM(1) PSSO_SWARM(2) PSSO_SWARM(3) PSSO_SWARM(4)
     PSSO_SWARM(5) PSSO_SWARM(6) PSSO_SWARM(7) PSSO_SWARM(8) PSSO_SWARM(9)
