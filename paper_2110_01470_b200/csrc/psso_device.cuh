@@ -978,6 +978,7 @@ __device__ __forceinline__ T chain_term1(T x, T nb, int e) {
 #define PSSO_CHAIN_PF 1  // FULL iteration kernel: TMA prefetch of the next group
 #endif
 
+
 // Shared-memory row stride of the chain kernels' per-warp prefetch buffer:
 // dense rows, so each array of a group arrives with ONE bulk copy (the four
 // 8-lane segments then share banks: 2x the minimum LDS wavefronts, cheaper
