@@ -744,10 +744,10 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
       c->fused_fn = f;
       c->rows_w = W;
       const int es = cfg->dtype == PSSO_F64 ? 8 : 4;
-      // gbest | warp reduction | leaf values [8/W][2][4W] | flags | mbarriers | prefetch buffers
+      // gbest | warp reduction | leaf values | mbarriers | prefetch buffers
       c->LF.off_red = (int)align16((size_t)(D + D / 16) * es);  // gbest padded per leaf
-      c->LF.off_leaf = c->LF.off_red + 128;
-      c->LF.off_flag = c->LF.off_leaf + 512;
+      c->LF.off_leaf = c->LF.off_red + 128;  // leaf values [2][8/W][2*4W + 1] doubles
+      c->LF.off_flag = c->LF.off_leaf + (int)align16(2 * (size_t)(8 / W) * (8 * W + 1) * 8);
       c->LF.off_bar = (int)align16((size_t)c->LF.off_flag + 32);
       c->LF.off_xs = (int)((c->LF.off_bar + 64 + 127) & ~127);
       c->LF.smem = (size_t)c->LF.off_xs + 8 * 8 * (size_t)128 * es;

@@ -1356,11 +1356,12 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, PSSO_CHAIN_MINB)
 // k_chain inside the leaf (lane k: j = 128*leaf + k + 8m, m < 16), so the
 // positions of the whole row stay in registers until the pBest decision:
 //   TMA-prefetched X/P slice -> keyed draw + select -> X streamed to HBM ->
-//   leaf chains + xor-shuffle combine -> leaf values to smem -> one warp per
-//   row combines the 4W leaves with a butterfly (xor 1, 2, ..., 2W: exactly
-//   the balanced tree, fp add being commutative) -> fitness, `<=`, p_f ->
-//   improved rows written to P from registers by all W warps.
-// Two CTA barriers per round; no atomics.  Objectives with position-local
+//   leaf chains + xor-shuffle combine -> leaf values to smem -> every warp
+//   of the row combines the 4W leaves with a butterfly (xor 1, 2, ..., 2W:
+//   exactly the balanced tree, fp add being commutative) -> fitness, `<=`
+//   -> its slice of an improved row written to P from registers; warp 0 of
+//   the row writes p_f and tracks the candidate.
+// One CTA barrier per round (leaf slots double-buffered); no atomics.  Objectives with position-local
 // terms (f1, f2, f5, f6, f9, probe).
 template <int FN>
 __host__ __device__ constexpr bool rows_fn() {
@@ -1376,8 +1377,7 @@ __global__ void __launch_bounds__(256, 2) k_rows(const __grid_constant__ TilePar
   T* gb = reinterpret_cast<T*>(smem);
   double* red_f = reinterpret_cast<double*>(smem + p.off_red);
   int64_t* red_i = reinterpret_cast<int64_t*>(smem + p.off_red + 8 * NW);
-  double* leafv = reinterpret_cast<double*>(smem + p.off_leaf);  // [RPC][2][NL]
-  int* flag = reinterpret_cast<int*>(smem + p.off_flag);          // [RPC]
+  double* leafv = reinterpret_cast<double*>(smem + p.off_leaf);  // [2][RPC][2 NL + 1]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = lane & 7, s = lane >> 3;
@@ -1425,12 +1425,15 @@ __global__ void __launch_bounds__(256, 2) k_rows(const __grid_constant__ TilePar
 
   double best_f = CUDART_INF;
   int64_t best_i = INT64_MAX;
-  for (int64_t r0 = (int64_t)blockIdx.x * RPC; r0 < rows; r0 += rstride) {  // CTA-uniform
+  int round = 0;
+  for (int64_t r0 = (int64_t)blockIdx.x * RPC; r0 < rows; r0 += rstride, ++round) {  // CTA-uniform
     const int64_t r = r0 + slot;
     const bool rv = r < rows;
     const int64_t gi = p.row_lo + r;
+    const int par = round & 1;
+    double* lv = leafv + (par * RPC + slot) * (2 * NL + 1);  // [s1 leaves][s2 leaves][x0]
     T x[M];
-    const double pf_row = (rv && sw == 0) ? p.p_f[r] : 0.0;  // needed after barrier A
+    const double pf_row = rv ? p.p_f[r] : 0.0;  // needed after barrier A
     if (rv) {
       T pv[M];
       mbar_wait(wbar, wphase);
@@ -1491,41 +1494,44 @@ __global__ void __launch_bounds__(256, 2) k_rows(const __grid_constant__ TilePar
         if constexpr (two_sums(FN)) a2 = N::add(a2, __shfl_xor_sync(0xffffffffu, a2, o));
       }
       if (k == 0) {
-        leafv[(slot * 2) * NL + 4 * sw + s] = (double)a1;
-        leafv[(slot * 2 + 1) * NL + 4 * sw + s] = (double)a2;
+        lv[4 * sw + s] = (double)a1;
+        lv[NL + 4 * sw + s] = (double)a2;
       }
+      if (sw == 0 && lane == 0) lv[2 * NL] = (double)x[0];
     }
-    __syncthreads();  // (A) all leaves of the CTA's rows are in smem
+    // (A) all leaves of the CTA's rows are in smem.  The only barrier per
+    // round: leaf slots are double-buffered by round parity, and every warp of
+    // a row combines the leaves itself, so nobody waits for a decision.
+    __syncthreads();
 
-    if (rv && sw == 0) {  // one warp per row: balanced tree over the 4W leaves
-      const T x0 = __shfl_sync(0xffffffffu, x[0], 0);
+    if (rv) {  // every warp of the row: balanced tree over the 4W leaves (redundant, no 2nd barrier)
+      const T x0 = (T)lv[2 * NL];
       T s1 = (T)0, s2 = (T)0;
       if (lane < NL) {
-        s1 = (T)leafv[(slot * 2) * NL + lane];
-        s2 = (T)leafv[(slot * 2 + 1) * NL + lane];
+        s1 = (T)lv[lane];
+        s2 = (T)lv[NL + lane];
       }
 #pragma unroll
       for (int o = 1; o < NL; o <<= 1) {
         s1 = N::add(s1, __shfl_xor_sync(0xffffffffu, s1, o));
         if constexpr (two_sums(FN)) s2 = N::add(s2, __shfl_xor_sync(0xffffffffu, s2, o));
       }
-      if (lane == 0) {
-        const double f = finish<T, FN>(s1, s2, (T)1, D, &x0, p.probe_level);
+      // lanes < 4W hold the row sums after the butterfly; lane 0 decides for all
+      const double f = finish<T, FN>(s1, s2, (T)1, D, &x0, p.probe_level);
+      const bool imp = __shfl_sync(0xffffffffu, (int)(f <= pf_row), 0) != 0;  // parallel.py:109
+      if (sw == 0 && lane == 0) {
         if (!isfinite(f) && p.bad)
           atomicMin(p.bad, ((unsigned long long)(t + 1) << 40) | (unsigned long long)gi);
         if (p.sol_f && ((mode & M_SOLF) || !isfinite(f))) p.sol_f[r] = f;
-        const bool imp = f <= pf_row;  // parallel.py:109, ties refresh
         const double pf = imp ? f : pf_row;
         if (imp) p.p_f[r] = f;
-        flag[slot] = imp;
         if (lex_less(pf, gi, best_f, best_i)) { best_f = pf; best_i = gi; }
       }
-    }
-    __syncthreads();  // (B) pbest decisions visible; leafv free for the next round
-    if (rv && flag[slot]) {
-      T* pr = P + r * (int64_t)D;
+      if (imp) {  // this warp's slice of pbests[i] = sol[i], from registers
+        T* pr = P + r * (int64_t)D;
 #pragma unroll
-      for (int m = 0; m < M; ++m) stg_stream<T, 1>(pr + jb + 8 * m, VecT<T, 1>{{x[m]}});
+        for (int m = 0; m < M; ++m) stg_stream<T, 1>(pr + jb + 8 * m, VecT<T, 1>{{x[m]}});
+      }
     }
   }
 
