@@ -451,6 +451,7 @@ TileParams tile_params(psso_ctx* c, int mode, int64_t t, const int64_t* t_dev, b
   p.var_min = c->cfg.var_min;
   p.span = c->cfg.var_max - c->cfg.var_min;
   p.span53 = std::ldexp(p.span, -53);
+  p.span64 = std::ldexp(p.span, -64);
   p.probe_level = c->cfg.probe_level;
   p.t_arg = t;
   p.t_dev = t_dev;

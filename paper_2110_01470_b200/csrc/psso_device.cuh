@@ -95,6 +95,7 @@ struct TileParams {
   uint64_t Kw32, Kp32, Kg32;   // philox mode: 32-bit word compared < K32
   double var_min, span;
   double span53;               // span * 2^-53 (fresh = var_min + k * span53, exact rescale)
+  double span64;               // span * 2^-64 (see fresh_offset)
   double probe_level;
   int64_t t_arg;
   const int64_t* t_dev;        // if non-null, the iteration is read from here
@@ -112,17 +113,48 @@ struct TileParams {
 
 // ------------------------------------------------------------------ RNG ----
 
-__device__ __forceinline__ uint64_t mix64(uint64_t z) {  // rng.py:48-52
-  z = (z ^ (z >> 30)) * MIX1;
-  z = (z ^ (z >> 27)) * MIX2;
+__device__ __forceinline__ uint64_t xs30(uint64_t z) { return z ^ (z >> 30); }
+// z * C mod 2^64 in three IMADs (lo*Clo wide, then the two cross terms added
+// straight into the high word); the C++ form costs a fourth (IADD) but has a
+// shorter dependency chain
+template <uint64_t C>
+__device__ __forceinline__ uint64_t mul64c(uint64_t z) {
+  uint64_t r;
+  asm("{\n\t.reg .u32 rl, rh;\n\t"
+      "mul.wide.u32 %0, %1, %3;\n\t"
+      "mov.b64 {rl, rh}, %0;\n\t"
+      "mad.lo.u32 rh, %1, %4, rh;\n\t"
+      "mad.lo.u32 rh, %2, %3, rh;\n\t"
+      "mov.b64 %0, {rl, rh};\n\t}"
+      : "=l"(r)
+      : "r"((uint32_t)z), "r"((uint32_t)(z >> 32)), "n"((uint32_t)C), "n"((uint32_t)(C >> 32)));
+  return r;
+}
+// mix64 after its first xorshift: mix64(z) == mix64_tail(xs30(z))
+// LEAN: the three-IMAD multiplies (fewer instructions, longer chain) --
+// measured faster where a lane holds few coordinates (M <= 8: C4), slower at
+// M = 16 (C3), where the four-IMAD form's parallel pair wins.
+template <bool LEAN = false>
+__device__ __forceinline__ uint64_t mix64_tail(uint64_t z) {
+  if constexpr (LEAN) {
+    z = mul64c<MIX1>(z);
+    z = mul64c<MIX2>(z ^ (z >> 27));
+  } else {
+    z *= MIX1;
+    z = (z ^ (z >> 27)) * MIX2;
+  }
   return z ^ (z >> 31);
 }
-__device__ __forceinline__ uint64_t xs30(uint64_t z) { return z ^ (z >> 30); }
-// mix64 after its first xorshift: mix64(z) == mix64_tail(xs30(z))
-__device__ __forceinline__ uint64_t mix64_tail(uint64_t z) {
-  z *= MIX1;
-  z = (z ^ (z >> 27)) * MIX2;
-  return z ^ (z >> 31);
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {  // rng.py:48-52 (SplitMix64 finalizer)
+  return mix64_tail(xs30(z));
+}
+// (h >> 11) * span * 2^-53 for h = mix64_tail(z), computed as
+// (h & ~0x7ff) * (span * 2^-64): the masked value converts to double exactly
+// and the power-of-two rescale is exact, so this equals the reference's
+// var_min + span*u offset bit for bit with the final shift folded away.
+template <bool LEAN = false>
+__device__ __forceinline__ double fresh_offset(uint64_t z, double span64) {
+  return __dmul_rn((double)(mix64_tail<LEAN>(z) & ~0x7ffull), span64);
 }
 __device__ __forceinline__ uint64_t fold64(uint64_t h, uint64_t f) {  // rng.py:55-58
   return mix64(h ^ (GAMMA * (f + 1)));
@@ -1068,9 +1100,8 @@ __device__ __forceinline__ void chain_step(const TileParams& p, const ChainEnv& 
       T v;
       if constexpr (RNG == 0) {
         const uint64_t gx = xg[j];
-        const uint64_t kb = mix64_tail(xb ^ gx) >> 11;
-        const double fresh =
-            __dadd_rn(p.var_min, __dmul_rn(p.span53, (double)(mix64_tail(xf ^ gx) >> 11)));
+        const uint64_t kb = mix64_tail<(M <= 8)>(xb ^ gx) >> 11;
+        const double fresh = __dadd_rn(p.var_min, fresh_offset<(M <= 8)>(xf ^ gx, p.span64));
         v = x[m];
         v = kb >= p.Kw ? pv[m] : v;
         v = kb >= p.Kp ? gb[j] : v;
@@ -1458,8 +1489,7 @@ __global__ void __launch_bounds__(256, 2) k_rows(const __grid_constant__ TilePar
           const int j = jb + 8 * m;
           const uint64_t gx = xs30(g0 + GAMMA * (uint64_t)(8 * m));
           const uint64_t kb = mix64_tail(xb ^ gx) >> 11;
-          const double fresh =
-              __dadd_rn(p.var_min, __dmul_rn(p.span53, (double)(mix64_tail(xf ^ gx) >> 11)));
+          const double fresh = __dadd_rn(p.var_min, fresh_offset(xf ^ gx, p.span64));
           T v = x[m];
           v = kb >= p.Kw ? pv[m] : v;
           v = kb >= p.Kp ? gbl[j] : v;
