@@ -656,6 +656,24 @@ cudaError_t launch_swarm(const SwarmPlan& pl, int64_t B, void** args, cudaStream
   return cudaLaunchKernel(pl.fn, dim3(1, (unsigned)B), dim3(PSSO_SWARM_NT), args, pl.smem, s);
 }
 
+// Stream-ordered allocations for the one-shot host-buffer entry points
+// (psso_solve, psso_solve_batch): the device's default memory pool keeps
+// freed blocks cached (release threshold = max), so repeated calls do not
+// pay for mapping and unmapping gigabytes of HBM.
+cudaError_t pool_alloc(void** p, size_t bytes, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    configured = true;
+  }
+  return cudaMallocAsync(p, bytes, s);
+}
+
 }  // namespace
 
 // ------------------------------------------------------------- C ABI ----
@@ -1231,20 +1249,20 @@ int psso_solve(const psso_config* cfg, int64_t niter, double* traj, void* best_p
   cudaError_t e = cudaSuccess;
   auto cleanup = [&]() {
     if (c) psso_destroy(c);
-    cudaFree(b.sol); cudaFree(b.pbests); cudaFree(b.p_f); cudaFree(b.gbest);
-    cudaFree(b.g_f); cudaFree(b.traj);
+    for (void* q : {b.sol, b.pbests, (void*)b.p_f, b.gbest, (void*)b.g_f, (void*)b.traj})
+      if (q) cudaFreeAsync(q, s);
     if (e0) cudaEventDestroy(e0);
     if (e1) cudaEventDestroy(e1);
-    if (s) cudaStreamDestroy(s);
+    if (s) { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
   };
   if ((e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) != cudaSuccess ||
       (e = cudaEventCreate(&e0)) != cudaSuccess || (e = cudaEventCreate(&e1)) != cudaSuccess ||
-      (e = cudaMalloc(&b.sol, N * D * es)) != cudaSuccess ||
-      (e = cudaMalloc(&b.pbests, N * D * es)) != cudaSuccess ||
-      (e = cudaMalloc((void**)&b.p_f, N * 8)) != cudaSuccess ||
-      (e = cudaMalloc(&b.gbest, D * es)) != cudaSuccess ||
-      (e = cudaMalloc((void**)&b.g_f, 8)) != cudaSuccess ||
-      (e = cudaMalloc((void**)&b.traj, (size_t)niter * 8)) != cudaSuccess) {
+      (e = pool_alloc(&b.sol, N * D * es, s)) != cudaSuccess ||
+      (e = pool_alloc(&b.pbests, N * D * es, s)) != cudaSuccess ||
+      (e = pool_alloc((void**)&b.p_f, N * 8, s)) != cudaSuccess ||
+      (e = pool_alloc(&b.gbest, D * es, s)) != cudaSuccess ||
+      (e = pool_alloc((void**)&b.g_f, 8, s)) != cudaSuccess ||
+      (e = pool_alloc((void**)&b.traj, (size_t)niter * 8, s)) != cudaSuccess) {
     cleanup();
     return cuda_fail(nullptr, e, "psso_solve alloc");
   }
@@ -1303,29 +1321,30 @@ int psso_solve_batch(const psso_config* cfg, const uint64_t* seeds, int32_t nsee
   cudaStream_t s = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   auto cleanup = [&]() {
-    for (Buf* b : {&X, &P, &pf, &gb, &gf, &tr, &ep, &sf, &si, &sn, &sr, &sd, &bad}) cudaFree(b->p);
+    for (Buf* b : {&X, &P, &pf, &gb, &gf, &tr, &ep, &sf, &si, &sn, &sr, &sd, &bad})
+      if (b->p) cudaFreeAsync(b->p, s);
     if (e0) cudaEventDestroy(e0);
     if (e1) cudaEventDestroy(e1);
-    if (s) cudaStreamDestroy(s);
+    if (s) { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
     psso_destroy(c);
   };
   if ((e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) != cudaSuccess ||
       (e = cudaEventCreate(&e0)) != cudaSuccess || (e = cudaEventCreate(&e1)) != cudaSuccess ||
-      (e = cudaMalloc(&X.p, B * N * D * es)) != cudaSuccess ||
-      (e = cudaMalloc(&P.p, B * N * D * es)) != cudaSuccess ||
-      (e = cudaMalloc(&pf.p, B * N * 8)) != cudaSuccess ||
-      (e = cudaMalloc(&gb.p, B * D * es)) != cudaSuccess ||
-      (e = cudaMalloc(&gf.p, B * 8)) != cudaSuccess ||
-      (e = cudaMalloc(&tr.p, B * (size_t)niter * 8)) != cudaSuccess ||
-      (e = cudaMalloc(&ep.p, B * 2 * G * sizeof(unsigned int))) != cudaSuccess ||
-      (e = cudaMalloc(&sf.p, B * 2 * G * 8)) != cudaSuccess ||
-      (e = cudaMalloc(&si.p, B * 2 * G * 8)) != cudaSuccess ||
-      (e = cudaMalloc(&sn.p, B * 2 * G * 4)) != cudaSuccess ||
-      (e = cudaMalloc(&sr.p, B * 2 * G * D * es)) != cudaSuccess ||
-      (e = cudaMalloc(&sd.p, B * 8)) != cudaSuccess ||
-      (e = cudaMalloc(&bad.p, B * 8)) != cudaSuccess ||
-      (e = cudaMemcpy(sd.p, seeds, B * 8, cudaMemcpyHostToDevice)) != cudaSuccess ||
-      (e = cudaMemset(bad.p, 0xff, B * 8)) != cudaSuccess) {
+      (e = pool_alloc(&X.p, B * N * D * es, s)) != cudaSuccess ||
+      (e = pool_alloc(&P.p, B * N * D * es, s)) != cudaSuccess ||
+      (e = pool_alloc(&pf.p, B * N * 8, s)) != cudaSuccess ||
+      (e = pool_alloc(&gb.p, B * D * es, s)) != cudaSuccess ||
+      (e = pool_alloc(&gf.p, B * 8, s)) != cudaSuccess ||
+      (e = pool_alloc(&tr.p, B * (size_t)niter * 8, s)) != cudaSuccess ||
+      (e = pool_alloc(&ep.p, B * 2 * G * sizeof(unsigned int), s)) != cudaSuccess ||
+      (e = pool_alloc(&sf.p, B * 2 * G * 8, s)) != cudaSuccess ||
+      (e = pool_alloc(&si.p, B * 2 * G * 8, s)) != cudaSuccess ||
+      (e = pool_alloc(&sn.p, B * 2 * G * 4, s)) != cudaSuccess ||
+      (e = pool_alloc(&sr.p, B * 2 * G * D * es, s)) != cudaSuccess ||
+      (e = pool_alloc(&sd.p, B * 8, s)) != cudaSuccess ||
+      (e = pool_alloc(&bad.p, B * 8, s)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(sd.p, seeds, B * 8, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
+      (e = cudaMemsetAsync(bad.p, 0xff, B * 8, s)) != cudaSuccess) {
     cleanup();
     return cuda_fail(nullptr, e, "psso_solve_batch alloc");
   }
