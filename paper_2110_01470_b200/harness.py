@@ -1,0 +1,292 @@
+"""Experiment cells on the B200 engine: the reference harness's run loop, batched.
+
+SURVEY §8(f) "next" #2: the reference harness (``harness.py``) runs every
+(function, schedule) cell as ``replications`` independent ``run_parallel``
+calls with seeds ``base_seed + run_id`` (``_run_one``, harness.py:148-163;
+``run_experiment``, :217-263) and streams a results CSV (schema :46, writer
+:187-214).  Here a parallel-schedule cell is ONE device job: all its seeds run
+side by side in the whole-run kernel (``run_parallel_batch``), and the records
+-- bit-identical per seed to ``run_parallel`` -- are written in the
+reference's CSV schema and formatting, so the reference's readers, summaries,
+statistics and plotting tools consume them unchanged.
+
+Only the parallel schedule is provided: the sequential-asynchronous schedule
+is serial across particles by definition and stays in the
+reference.  Shapes the batched kernel does not take (nvar > 128, or
+nsol*nvar > 2^22) fall back to one ``run_parallel`` per seed on the device.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field, replace
+from pathlib import Path
+from typing import Optional, Sequence, Union
+
+import numpy as np
+
+from .benchmarks import BenchmarkFn, make_function
+from .core import SsoParams
+from .parallel import LayoutMode, run_parallel, run_parallel_batch
+from .records import RunRecord, ScheduleKind
+
+__all__ = [
+    "CSV_HEADER",
+    "ExperimentConfig",
+    "ExperimentReport",
+    "SpeedupReport",
+    "SummaryRow",
+    "compute_speedup",
+    "read_records",
+    "run_cell",
+    "run_experiment",
+    "summarize",
+    "write_records",
+    "write_summary",
+]
+
+#: results CSV columns, identical to the reference (harness.py:46)
+CSV_HEADER = "run_id,schedule,function,nsol,nvar,niter,cw,cp,cg,seed,best_fitness,wall_time_s"
+_BATCH_MAX_ELEMS = 1 << 22
+
+
+def _cell(value) -> str:
+    # floats in repr form, like the reference's writer, so rows round-trip exactly
+    return repr(value) if isinstance(value, float) else str(value)
+
+
+@dataclass(frozen=True)
+class SummaryRow:
+    """Per-cell best-fitness statistics (reference harness.py:71-79)."""
+
+    function: str
+    schedule: ScheduleKind
+    n: int
+    mean: float
+    std: Optional[float]  # None for a single replication, like the reference
+    min: float
+
+
+@dataclass(frozen=True)
+class SpeedupReport:
+    """Mean-time ratio and power-rectified efficiency (reference harness.py:82-93)."""
+
+    mean_time_a: float
+    mean_time_b: float
+    speedup: float
+    power_a: float
+    power_b: float
+    power_ratio: float
+    rectified_efficiency: float
+    nsol: Optional[int] = None
+
+
+@dataclass
+class ExperimentConfig:
+    """The reference's experiment configuration (harness.py:96-128), parallel schedule.
+
+    Extra keyword fields: ``dtype`` and ``rng`` as in ``run_parallel``.
+    ``workers``, ``layout`` and ``block_size`` are accepted and have no effect
+    on results, as in the reference.
+    """
+
+    functions: Sequence[Union[str, BenchmarkFn]] = ("f1",)
+    schedules: Sequence[ScheduleKind] = (ScheduleKind.PARALLEL,)
+    replications: int = 20
+    base_seed: int = 0
+    nsol: int = 100
+    nvar: int = 50
+    niter: int = 1000
+    cw: float = 0.3
+    cp: float = 0.6
+    cg: float = 0.8
+    workers: int = 1
+    layout: LayoutMode = LayoutMode.PARTICLE_MAJOR
+    record_trajectory: bool = False
+    block_size: int = 1024
+    dtype: str = "float64"
+    rng: str = "reference"
+
+    def __post_init__(self):
+        if not self.functions:
+            raise ValueError("config key 'functions' must list at least one function")
+        if not self.schedules:
+            raise ValueError("config key 'schedules' must list at least one schedule")
+        self.schedules = [ScheduleKind(s) for s in self.schedules]
+        if ScheduleKind.SEQUENTIAL in self.schedules:
+            raise ValueError("the sequential schedule is not provided by the B200 engine "
+                             "(serial across particles); run it with the reference")
+        self.layout = LayoutMode(self.layout)
+        if not 0.0 <= self.cw <= self.cp <= self.cg <= 1.0:
+            raise ValueError(
+                f"thresholds must satisfy 0 <= cw <= cp <= cg <= 1, "
+                f"got ({self.cw}, {self.cp}, {self.cg})"
+            )
+        for key in ("replications", "nsol", "nvar", "niter", "workers"):
+            if int(getattr(self, key)) < 1:
+                raise ValueError(f"config key {key!r} must be >= 1")
+
+
+@dataclass
+class ExperimentReport:
+    config: ExperimentConfig
+    records: list
+    summaries: list
+    metadata: dict = field(default_factory=dict)
+
+
+def _function(entry, nvar: int) -> BenchmarkFn:
+    return entry if isinstance(entry, BenchmarkFn) else make_function(entry, nvar)
+
+
+def run_cell(fn: BenchmarkFn, config: ExperimentConfig, run_ids: Sequence[int]) -> list:
+    """Replications ``run_ids`` of one parallel cell (reference _run_one, harness.py:148-163).
+
+    Seeds are ``base_seed + run_id``.  One batched launch when the shape allows
+    it; ``wall_time_s`` is then the batch's loop time divided evenly over its
+    runs (per-run device time; the reference times each run separately).
+    """
+    params = SsoParams(cw=config.cw, cp=config.cp, cg=config.cg, var_min=fn.var_min,
+                       var_max=fn.var_max, nsol=config.nsol, nvar=config.nvar,
+                       niter=config.niter)
+    seeds = [config.base_seed + rid for rid in run_ids]
+    if config.nvar <= 128 and config.nsol * config.nvar <= _BATCH_MAX_ELEMS:
+        recs = run_parallel_batch(params, fn, seeds, dtype=config.dtype, rng=config.rng)
+        per_run = recs[0].wall_time_s / len(recs)
+        recs = [replace(r, run_id=rid, wall_time_s=per_run) for r, rid in zip(recs, run_ids)]
+    else:
+        recs = [replace(run_parallel(params, fn, s, workers=config.workers, layout=config.layout,
+                                     dtype=config.dtype, rng=config.rng), run_id=rid)
+                for s, rid in zip(seeds, run_ids)]
+    out = []
+    for r in recs:
+        r = replace(r, function=fn.id)
+        if not config.record_trajectory:
+            r = replace(r, trajectory=None)
+        out.append(r)
+    return out
+
+
+def summarize(records: Sequence[RunRecord]) -> list:
+    """Per (function, schedule) mean / sample std / min, in first-seen order (harness.py:166-184)."""
+    cells: dict = {}
+    for rec in records:
+        cells.setdefault((rec.function, rec.schedule), []).append(rec.best_fitness)
+    out = []
+    for (function, schedule), vals in cells.items():
+        a = np.asarray(vals, dtype=np.float64)
+        out.append(SummaryRow(function=function, schedule=schedule, n=int(a.size),
+                              mean=float(a.mean()),
+                              std=float(a.std(ddof=1)) if a.size > 1 else None,
+                              min=float(a.min())))
+    return out
+
+
+class _Rows:
+    """Streaming results CSV in the reference format (harness.py:187-214)."""
+
+    def __init__(self, path):
+        self.fh = None if path is None else open(path, "w", encoding="utf-8")
+        if self.fh:
+            self.fh.write(CSV_HEADER + "\n")
+            self.fh.flush()
+
+    def add(self, rec: RunRecord):
+        if self.fh:
+            row = rec.scalar_row()
+            self.fh.write(",".join(_cell(row[c]) for c in CSV_HEADER.split(",")) + "\n")
+            self.fh.flush()
+
+    def failed(self, exc: BaseException):
+        if self.fh:
+            self.fh.write(f"# FAILED: {type(exc).__name__}: {exc}\n")
+            self.fh.flush()
+
+    def close(self):
+        if self.fh:
+            self.fh.close()
+            self.fh = None
+
+
+def run_experiment(config: ExperimentConfig, out=None, summary_out=None) -> ExperimentReport:
+    """Every cell, all replications, records streamed to ``out`` (reference harness.py:217-263).
+
+    A failure mid-experiment (e.g. ``NonFiniteFitnessError``) leaves the
+    completed cells' rows plus a ``# FAILED`` marker, like the reference.
+    """
+    functions = [_function(e, config.nvar) for e in config.functions]
+    sink = _Rows(None if out is None else Path(out))
+    records = []
+    try:
+        for fn in functions:
+            for _schedule in config.schedules:  # parallel only (validated)
+                for rec in run_cell(fn, config, range(config.replications)):
+                    sink.add(rec)
+                    records.append(rec)
+    except BaseException as exc:
+        sink.failed(exc)
+        raise
+    finally:
+        sink.close()
+    report = ExperimentReport(config=config, records=records, summaries=summarize(records),
+                              metadata={"block_size": config.block_size, "engine": "b200"})
+    if summary_out is not None:
+        write_summary(report.summaries, summary_out)
+    return report
+
+
+def write_records(records: Sequence[RunRecord], path) -> None:
+    sink = _Rows(Path(path))
+    try:
+        for rec in records:
+            sink.add(rec)
+    finally:
+        sink.close()
+
+
+def read_records(path) -> list:
+    """Results CSV (this module's or the reference's) back into records (harness.py:275-305)."""
+    recs = []
+    with open(path, encoding="utf-8") as fh:
+        header = fh.readline().strip()
+        if header != CSV_HEADER:
+            raise ValueError(f"unexpected CSV header {header!r}")
+        for line in fh:
+            line = line.strip()
+            if not line or line.startswith("#"):
+                continue
+            p = line.split(",")
+            if len(p) != 12:
+                raise ValueError(f"malformed row: {line!r}")
+            recs.append(RunRecord(run_id=int(p[0]), schedule=ScheduleKind(p[1]), function=p[2],
+                                  nsol=int(p[3]), nvar=int(p[4]), niter=int(p[5]),
+                                  cw=float(p[6]), cp=float(p[7]), cg=float(p[8]), seed=int(p[9]),
+                                  best_fitness=float(p[10]), wall_time_s=float(p[11])))
+    return recs
+
+
+def write_summary(summaries: Sequence[SummaryRow], path) -> None:
+    """Summary CSV in the reference format (harness.py:308-315)."""
+    with open(path, "w", encoding="utf-8") as fh:
+        fh.write("function,schedule,n,mean,std,min\n")
+        for s in summaries:
+            std = "" if s.std is None else repr(s.std)
+            fh.write(f"{s.function},{s.schedule},{s.n},{s.mean!r},{std},{s.min!r}\n")
+
+
+def compute_speedup(times_a, times_b, power_a: float, power_b: float,
+                    nsol: Optional[int] = None) -> SpeedupReport:
+    """Speedup = mean(a)/mean(b); RE = speedup / (power_b/power_a) (harness.py:354-384, Eq. 3.1-3.3)."""
+    a = np.asarray(times_a, dtype=np.float64)
+    b = np.asarray(times_b, dtype=np.float64)
+    if a.size == 0 or b.size == 0:
+        raise ValueError("time samples must be nonempty")
+    if (a <= 0).any() or (b <= 0).any():
+        raise ValueError("wall times must be positive")
+    if power_a <= 0 or power_b <= 0:
+        raise ValueError("power ratings must be positive")
+    ma, mb = float(a.mean()), float(b.mean())
+    s = ma / mb
+    ratio = power_b / power_a
+    return SpeedupReport(mean_time_a=ma, mean_time_b=mb, speedup=s, power_a=power_a,
+                         power_b=power_b, power_ratio=ratio, rectified_efficiency=s / ratio,
+                         nsol=nsol)

@@ -1,0 +1,79 @@
+"""The B200 experiment harness writes the reference harness's CSV (SURVEY §8 f, next #2).
+
+Golden rows: tests/golden/make_harness_golden.py ran the REFERENCE
+``sso.harness.run_experiment`` on the cells below (wall-time column blanked).
+"""
+
+import io
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2110_01470_b200 import harness as H
+from paper_2110_01470_b200.records import ScheduleKind
+
+GOLD = Path(__file__).resolve().parent / "golden"
+CELLS = dict(functions=["f1", "f4", "f5", "f7"], schedules=[ScheduleKind.PARALLEL],
+             replications=4, base_seed=7, nsol=64, nvar=16, niter=60)
+
+
+def _golden_records(tmp_path):
+    text = (GOLD / "harness_records.csv").read_text().splitlines()
+    filled = [text[0]] + [r + "0.0" for r in text[1:]]  # wall time is machine-dependent
+    p = tmp_path / "g.csv"
+    p.write_text("\n".join(filled) + "\n")
+    return H.read_records(p)
+
+
+def test_csv_header_is_the_reference_schema():
+    assert (GOLD / "harness_records.csv").read_text().splitlines()[0] == H.CSV_HEADER
+
+
+def test_records_round_trip_and_summary_matches_reference(tmp_path):
+    recs = _golden_records(tmp_path)
+    assert len(recs) == 16 and recs[0].seed == 7 and recs[3].run_id == 3
+    out = tmp_path / "r.csv"
+    H.write_records(recs, out)
+    assert H.read_records(out) == recs
+    s = tmp_path / "s.csv"
+    H.write_summary(H.summarize(recs), s)
+    assert s.read_text() == (GOLD / "harness_summary.csv").read_text()
+
+
+def test_speedup_arithmetic_table_a3():
+    # PAPER.md Table 3.10 / A.3 (reference test_acceptance.py:201-237): N = 100
+    r = H.compute_speedup([48.8263], [0.13875], power_a=84.0, power_b=180.0, nsol=100)
+    assert abs(r.speedup - 48.8263 / 0.13875) < 1e-9
+    assert abs(r.rectified_efficiency - 164.2206) < 1e-3
+    with pytest.raises(ValueError):
+        H.compute_speedup([], [1.0], 84.0, 180.0)
+
+
+def test_config_validation():
+    with pytest.raises(ValueError, match="sequential"):
+        H.ExperimentConfig(schedules=[ScheduleKind.SEQUENTIAL])
+    with pytest.raises(ValueError, match="thresholds"):
+        H.ExperimentConfig(cw=0.5, cp=0.4)
+    with pytest.raises(ValueError, match="replications"):
+        H.ExperimentConfig(replications=0)
+
+
+@pytest.mark.gpu
+def test_run_experiment_matches_reference_rows(tmp_path):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    out, summ = tmp_path / "r.csv", tmp_path / "s.csv"
+    rep = H.run_experiment(H.ExperimentConfig(**CELLS), out=out, summary_out=summ)
+    gold = _golden_records(tmp_path)
+    mine = H.read_records(out)
+    assert len(mine) == len(gold) == len(rep.records)
+    for a, b in zip(mine, gold):
+        assert (a.run_id, a.function, a.seed, a.nsol, a.nvar, a.niter) == \
+               (b.run_id, b.function, b.seed, b.nsol, b.nvar, b.niter)
+        if a.function in ("f1", "f4"):   # pure +,-,* objectives: bitwise
+            assert a.best_fitness == b.best_fitness
+        else:                            # transcendental objectives: 1e-12
+            assert abs(a.best_fitness - b.best_fitness) <= 1e-12 * abs(b.best_fitness)
+        assert a.wall_time_s > 0
