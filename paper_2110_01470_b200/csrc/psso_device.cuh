@@ -1097,6 +1097,9 @@ __device__ __forceinline__ void chain_step(const TileParams& p, const ChainEnv& 
 #pragma unroll
     for (int m = 0; m < M; ++m) {
       const int j = k + 8 * m;
+      // rows shorter than 8M (C2: D = 100 in M = 16) skip the empty tail
+      // columns with a warp-uniform branch instead of computing and dropping them
+      if (!FULL && 8 * m >= D) break;
       T v;
       if constexpr (RNG == 0) {
         const uint64_t gx = xg[j];
@@ -1123,7 +1126,7 @@ __device__ __forceinline__ void chain_step(const TileParams& p, const ChainEnv& 
     for (int m = 0; m < M; ++m) {
       const int j = k + 8 * m;
       if (FULL || j < D) {
-        if constexpr (FN == 7) row[j] = N::cos_(N::mul(x[m], (T)p.aux[j]));  // factors
+        if constexpr (FN == 7) row[j] = Trig<T>::cos_(N::mul(x[m], (T)p.aux[j]));  // factors
         else row[j] = x[m];
       }
     }

@@ -66,6 +66,23 @@ template <> struct Trig<double> {
     const double p = cos2pi_abs(x, odd);
     return flip(p, odd);
   }
+  // cos(y), |y| < 2^40: k = rint(y/pi), r = y - k*pi (two-constant Cody-Waite),
+  // cos(y) = (-1)^k cos(pi * s) with s = r/pi, |s| <= 1/2 -- the cos(pi s)
+  // polynomial again (f7's cos(x_j / sqrt(j)))
+  static __device__ __forceinline__ double cos_(double y) {
+    const double M = 6755399441055744.0;
+    const double t = __fma_rn(y, 0.3183098861837907, M);  // 1/pi
+    const double kd = __dsub_rn(t, M);
+    const uint32_t odd = (uint32_t)__double2loint(t) << 31;
+    double r = __fma_rn(-kd, 3.141592653589793, y);
+    r = __fma_rn(-kd, 1.2246467991473532e-16, r);
+    const double sp = __dmul_rn(r, 0.3183098861837907);
+    const double z = __dmul_rn(sp, sp);
+    double p = kCosPiD[9];
+#pragma unroll
+    for (int i = 8; i >= 0; --i) p = __fma_rn(p, z, kCosPiD[i]);
+    return flip(p, odd);
+  }
   static __device__ __forceinline__ double sin_(double w) {
     const double M = 6755399441055744.0;
     const double t = __fma_rn(w, 0.3183098861837907, M);  // 1/pi
@@ -100,6 +117,20 @@ template <> struct Trig<float> {
   static __device__ __forceinline__ float cos2pi(float x) {
     uint32_t odd;
     const float p = cos2pi_abs(x, odd);
+    return flip(p, odd);
+  }
+  static __device__ __forceinline__ float cos_(float y) {
+    const float M = 12582912.0f;
+    const float t = __fmaf_rn(y, 0.31830987334251404f, M);
+    const float kd = __fsub_rn(t, M);
+    const uint32_t odd = (uint32_t)__float_as_uint(t) << 31;
+    float r = __fmaf_rn(-kd, 3.1415927410125732f, y);
+    r = __fmaf_rn(-kd, -8.742277657347586e-08f, r);
+    const float sp = __fmul_rn(r, 0.31830987334251404f);
+    const float z = __fmul_rn(sp, sp);
+    float p = kCosPiF[5];
+#pragma unroll
+    for (int i = 4; i >= 0; --i) p = __fmaf_rn(p, z, kCosPiF[i]);
     return flip(p, odd);
   }
   static __device__ __forceinline__ float sin_(float w) {
