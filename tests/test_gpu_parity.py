@@ -556,3 +556,39 @@ def test_batch_nonfinite_names_particle():
     with pytest.raises(psso.NonFiniteFitnessError) as ei:
         psso.run_parallel_batch(p, fn, [0, 1, 2])
     assert ei.value.particle >= 0
+
+
+# ------------------------------------------------- kernel dispatch paths ----
+
+@pytest.mark.parametrize("fid,nsol,nvar,box,kernel", [
+    ("f5", 1 << 16, 128, None, "k_chain"),       # streaming, register rows
+    ("f5", 1000, 100, None, "k_swarm"),          # small swarm: whole run in one launch
+    ("f6", 300, 1024, None, "k_rows"),           # long rows D = 512 W
+    ("f5", 300, 300, None, "k_fused"),           # D > 128, not 512 W: TMA tile ring
+    ("f5", 200, 301, None, "k_tile"),            # odd row length: register tiles
+    ("f5", 1 << 16, 128, 1e13, "k_fused"),       # box beyond the branch-free trig range
+    ("f9", 500, 63, 1e13, "k_tile"),
+])
+def test_dispatch_paths_against_oracle(fid, nsol, nvar, box, kernel):
+    """Every iteration-kernel family, selected by shape, against the oracle."""
+    fn = _fn(fid, nvar)
+    niter = 4
+    p = _params(fn, nsol, niter, var_min=None if box is None else -box,
+                var_max=None if box is None else box)
+    eng = DeviceEngine(p, fn, 5, keep_sol_f=True)
+    try:
+        name = _lib.load().psso_kernel_name(eng.ctx).decode()
+        assert name.startswith(kernel), name
+        eng.initialize()
+        eng.run(0, niter)
+        eng.check()
+        sw = eng.to_host()
+        traj = eng.traj.cpu().numpy()
+    finally:
+        eng.close()
+    o = O.Oracle.from_params(p, fid, 5, threads=O.max_threads())
+    osw = o.initialize()
+    otraj = o.run(osw, 0, niter)
+    assert np.array_equal(sw.sol, osw.sol) and np.array_equal(sw.pbests, osw.pbests)
+    assert np.array_equal(sw.gbest, osw.gbest)
+    assert _close(sw.p_f, osw.p_f, fid) and _close(traj, otraj, fid)
