@@ -1058,6 +1058,24 @@ __device__ __forceinline__ void chain_step(const TileParams& p, const ChainEnv& 
   const int mode = INIT ? (M_INIT | M_EVAL | M_CAND | M_SOLF)
                         : (M_SEARCH | M_EVAL | M_PBEST | M_CAND | (p.mode & M_SOLF));
 
+  // fitness accumulators: lane k sums terms k, k+8, ... in order (numpy's r[k])
+  T a1 = (T)0, a2 = (T)0, t1 = (T)0, t2 = (T)0;
+  auto add_term = [&](int m, T v1, T v2) {
+    if (m < ev.mlen) {
+      a1 = (m == 0) ? v1 : N::add(a1, v1);
+      if constexpr (two_sums(FN)) a2 = (m == 0) ? v2 : N::add(a2, v2);
+    } else if (m == ev.mlen && k < ev.tail) {
+      t1 = v1;
+      t2 = v2;
+    }
+  };
+  // position-local objectives: each coordinate's terms right after its draw,
+  // interleaving the integer-heavy hash with the fp64-heavy terms.  Measured:
+  // a win for latency-bound rows (k_swarm, C2: 7.9 -> 7.6 us/iteration), a
+  // loss for the HBM-streaming FULL kernels (C3 0.548 -> 0.561 ms), which
+  // keep the two-phase schedule.
+  constexpr bool FUSE = !INIT && !FULL && FN != 4 && !chain_smem_fn<FN>();
+
   // ---- positions
   if constexpr (INIT) {
     uint64_t hb = 0;
@@ -1115,6 +1133,12 @@ __device__ __forceinline__ void chain_step(const TileParams& p, const ChainEnv& 
       }
       x[m] = v;
       if (rv && (FULL || j < D)) st_row<T, RES>(xr + j, v);
+      if constexpr (FUSE) {
+        const T v1 = chain_term1<T, FN>(v, (T)0, j);
+        T v2 = (T)0;
+        if constexpr (two_sums(FN)) v2 = Trig<T>::cos2pi(v);
+        add_term(m, v1, v2);
+      }
     }
   }
 
@@ -1148,30 +1172,25 @@ __device__ __forceinline__ void chain_step(const TileParams& p, const ChainEnv& 
     }
   }
 
-  // ---- fitness: lane k accumulates terms k, k+8, ... in order
-  T a1 = (T)0, a2 = (T)0, t1 = (T)0, t2 = (T)0;
+  // ---- fitness terms (INIT, f4's neighbour, the smem-row objectives)
+  if constexpr (!FUSE) {
 #pragma unroll
-  for (int m = 0; m < M; ++m) {
-    const int e = k + 8 * m;
-    T nb = (T)0;
-    if constexpr (FN == 4) {
-      const T nxt = (m + 1 < M) ? x[m + 1 < M ? m + 1 : m] : (T)0;
-      const T prov = (k == 0) ? nxt : x[m];
-      nb = __shfl_sync(0xffffffffu, prov, k < 7 ? lane + 1 : lane - 7);
-    }
-    if (m < ev.mlen || (m == ev.mlen && k < ev.tail)) {
-      T v1;
-      if constexpr (FN == 3) v1 = row[e];
-      else if constexpr (FN == 8) v1 = heavy_term<T, 8>(row, e);
-      else v1 = chain_term1<T, FN>(x[m], nb, e);
-      T v2 = (T)0;
-      if constexpr (two_sums(FN)) v2 = Trig<T>::cos2pi(x[m]);
-      if (m < ev.mlen) {
-        a1 = (m == 0) ? v1 : N::add(a1, v1);
-        if constexpr (two_sums(FN)) a2 = (m == 0) ? v2 : N::add(a2, v2);
-      } else {
-        t1 = v1;
-        t2 = v2;
+    for (int m = 0; m < M; ++m) {
+      const int e = k + 8 * m;
+      T nb = (T)0;
+      if constexpr (FN == 4) {
+        const T nxt = (m + 1 < M) ? x[m + 1 < M ? m + 1 : m] : (T)0;
+        const T prov = (k == 0) ? nxt : x[m];
+        nb = __shfl_sync(0xffffffffu, prov, k < 7 ? lane + 1 : lane - 7);
+      }
+      if (m < ev.mlen || (m == ev.mlen && k < ev.tail)) {
+        T v1;
+        if constexpr (FN == 3) v1 = row[e];
+        else if constexpr (FN == 8) v1 = heavy_term<T, 8>(row, e);
+        else v1 = chain_term1<T, FN>(x[m], nb, e);
+        T v2 = (T)0;
+        if constexpr (two_sums(FN)) v2 = Trig<T>::cos2pi(x[m]);
+        add_term(m, v1, v2);
       }
     }
   }
@@ -1483,8 +1502,20 @@ __global__ void __launch_bounds__(256, 2) k_rows(const __grid_constant__ TilePar
       fence_proxy_async();
       prefetch(r + rstride);
 
-      // ---- positions (core.py:138-173; see k_chain)
+      // ---- positions (core.py:138-173; see k_chain), each followed at once
+      // by its objective terms and the in-order chain adds of leaf 4sw+s
+      // (lane k: r[k]) -- interleaving the integer-heavy draw with the
+      // fp64-heavy terms keeps both pipes busy
       T* xr = X + r * (int64_t)D;
+      T a1 = (T)0, a2 = (T)0;
+      auto accumulate = [&](int m, T v) {
+        const T v1 = chain_term1<T, FN>(v, (T)0, jb + 8 * m);
+        a1 = m == 0 ? v1 : N::add(a1, v1);
+        if constexpr (two_sums(FN)) {
+          const T v2 = Trig<T>::cos2pi(v);
+          a2 = m == 0 ? v2 : N::add(a2, v2);
+        }
+      };
       if constexpr (RNG == 0) {
         const uint64_t xb = xs30(fold64(rootb, (uint64_t)gi)), xf = xs30(fold64(rootf, (uint64_t)gi));
 #pragma unroll
@@ -1499,6 +1530,7 @@ __global__ void __launch_bounds__(256, 2) k_rows(const __grid_constant__ TilePar
           v = kb >= p.Kg ? (T)fresh : v;
           x[m] = v;
           stg_stream<T, 1>(xr + j, VecT<T, 1>{{v}});
+          accumulate(m, v);
         }
       } else {
 #pragma unroll
@@ -1507,20 +1539,10 @@ __global__ void __launch_bounds__(256, 2) k_rows(const __grid_constant__ TilePar
           VecT<T, 1> xv{{x[m]}}, pb{{pv[m]}}, gv{{gbl[j]}};
           x[m] = search_chunk<T, 1, 1>(p, xv, pb, gv, 0, 0, j, (uint64_t)gi, t, p.seed).v[0];
           stg_stream<T, 1>(xr + j, VecT<T, 1>{{x[m]}});
+          accumulate(m, x[m]);
         }
       }
 
-      // ---- leaf chains (lane k: r[k] of leaf 4sw+s) and the 8-lane combine
-      T a1 = (T)0, a2 = (T)0;
-#pragma unroll
-      for (int m = 0; m < M; ++m) {
-        const T v1 = chain_term1<T, FN>(x[m], (T)0, jb + 8 * m);
-        a1 = m == 0 ? v1 : N::add(a1, v1);
-        if constexpr (two_sums(FN)) {
-          const T v2 = Trig<T>::cos2pi(x[m]);
-          a2 = m == 0 ? v2 : N::add(a2, v2);
-        }
-      }
 #pragma unroll
       for (int o = 1; o < 8; o <<= 1) {
         a1 = N::add(a1, __shfl_xor_sync(0xffffffffu, a1, o));
