@@ -131,9 +131,10 @@ __device__ __forceinline__ uint64_t mul64c(uint64_t z) {
   return r;
 }
 // mix64 after its first xorshift: mix64(z) == mix64_tail(xs30(z))
-// LEAN: the three-IMAD multiplies (fewer instructions, longer chain) --
-// measured faster where a lane holds few coordinates (M <= 8: C4), slower at
-// M = 16 (C3), where the four-IMAD form's parallel pair wins.
+// LEAN: the three-IMAD multiplies (fewer instructions, longer chain).  Measured
+// (sustained 500-iteration runs, where the board's power cap binds): faster
+// for fp64 at every M (C3 0.565 -> 0.559 ms, C4) and for M <= 8; slower for
+// fp32 at M = 16 (issue-bound: the four-IMAD form's parallel pair wins).
 template <bool LEAN = false>
 __device__ __forceinline__ uint64_t mix64_tail(uint64_t z) {
   if constexpr (LEAN) {
@@ -1121,8 +1122,8 @@ __device__ __forceinline__ void chain_step(const TileParams& p, const ChainEnv& 
       T v;
       if constexpr (RNG == 0) {
         const uint64_t gx = xg[j];
-        const uint64_t kb = mix64_tail<(M <= 8)>(xb ^ gx) >> 11;
-        const double fresh = __dadd_rn(p.var_min, fresh_offset<(M <= 8)>(xf ^ gx, p.span64));
+        const uint64_t kb = mix64_tail<(M <= 8 || sizeof(T) == 8)>(xb ^ gx) >> 11;
+        const double fresh = __dadd_rn(p.var_min, fresh_offset<(M <= 8 || sizeof(T) == 8)>(xf ^ gx, p.span64));
         v = x[m];
         v = kb >= p.Kw ? pv[m] : v;
         v = kb >= p.Kp ? gb[j] : v;
