@@ -1523,8 +1523,8 @@ __global__ void __launch_bounds__(256, 2) k_rows(const __grid_constant__ TilePar
         for (int m = 0; m < M; ++m) {
           const int j = jb + 8 * m;
           const uint64_t gx = xs30(g0 + GAMMA * (uint64_t)(8 * m));
-          const uint64_t kb = mix64_tail(xb ^ gx) >> 11;
-          const double fresh = __dadd_rn(p.var_min, fresh_offset(xf ^ gx, p.span64));
+          const uint64_t kb = mix64_tail<(sizeof(T) == 8)>(xb ^ gx) >> 11;
+          const double fresh = __dadd_rn(p.var_min, fresh_offset<(sizeof(T) == 8)>(xf ^ gx, p.span64));
           T v = x[m];
           v = kb >= p.Kw ? pv[m] : v;
           v = kb >= p.Kp ? gbl[j] : v;
