@@ -14,7 +14,7 @@ for w in ${WORKLOADS:-c3 c3f32 c4}; do
 import json
 for l in open('gpurun_out/ab.log'):
   if l.startswith('{'):
-    d=json.loads(l); r=d['roofline']; print('$w', '$lib', 'ms %.4f'%r['kernel_ms_per_iteration'], 'frac %.3f'%r['frac'])
+    d=json.loads(l); r=d['roofline']; print('$w', '$lib', 'kernel ms %.4f'%r['kernel_ms_per_iteration'], 'step ms %.4f'%d['ms_per_step'], 'frac %.3f'%r['frac'])
 " || tail -3 gpurun_out/ab.log
     done
   done
