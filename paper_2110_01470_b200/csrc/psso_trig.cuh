@@ -4,11 +4,11 @@
 // :165-166 sin(sqrt|x|)) dominate the issue budget of the fused iteration
 // once the keyed hash is paid for.  These versions use an exact argument
 // reduction and one near-minimax polynomial (coefficients from
-// scripts/fit_trig.py, max abs error 7.9e-17 / 3.8e-17 in fp64 before
+// scripts/fit_trig.py, max abs error 1.4e-16 / 3.8e-17 in fp64 before
 // rounding of the Horner steps), no range branch and no libdevice call:
 //
 //   cos(2*pi*x):  s = 2x - rint(2x) exactly (|s| <= 1/2),
-//                 cos(2*pi*x) = (-1)^rint(2x) * P(s^2)        -- 13 fp64 ops
+//                 cos(2*pi*x) = (-1)^rint(2x) * P(s^2)        -- 12 fp64 ops
 //   sin(w):       r = w - k*pi (two-constant Cody-Waite, FMA), |r| <= pi/2,
 //                 sin(w) = (-1)^k * r * Q(r^2)                 -- 15 fp64 ops
 //
@@ -26,10 +26,9 @@
 namespace psso {
 
 // cos(pi*s) = P(s^2), |s| <= 1/2
-static __constant__ double kCosPiD[10] = {
-    1.0, -4.934802200544679, 4.058712126416768, -1.335262768854555, 0.2353306303579955,
-    -0.025806891376598716, 0.0019295741873202796, -0.0001046374169719714,
-    4.300724502204995e-06, -1.3435242235366654e-07};
+static __constant__ double kCosPiD[9] = {
+    1.0, -4.934802200544676, 4.058712126416498, -1.335262768843456, 0.23533063012967062,
+    -0.02580688873817758, 0.001929556278037417, -0.00010456656706174584, 4.149578027057121e-06};
 static __constant__ float kCosPiF[6] = {1.0f, -4.934802055358887f, 4.058709144592285f,
                                         -1.335211992263794f, 0.23493731021881104f,
                                         -0.024396324530243874f};
@@ -53,9 +52,9 @@ template <> struct Trig<double> {
     odd = (uint32_t)__double2loint(t) << 31;
     const double s = __fma_rn(x, 2.0, -kd);  // exact
     const double z = __dmul_rn(s, s);
-    double p = kCosPiD[9];
+    double p = kCosPiD[8];
 #pragma unroll
-    for (int i = 8; i >= 0; --i) p = __fma_rn(p, z, kCosPiD[i]);
+    for (int i = 7; i >= 0; --i) p = __fma_rn(p, z, kCosPiD[i]);
     return p;
   }
   static __device__ __forceinline__ double flip(double v, uint32_t odd) {
@@ -78,9 +77,9 @@ template <> struct Trig<double> {
     r = __fma_rn(-kd, 1.2246467991473532e-16, r);
     const double sp = __dmul_rn(r, 0.3183098861837907);
     const double z = __dmul_rn(sp, sp);
-    double p = kCosPiD[9];
+    double p = kCosPiD[8];
 #pragma unroll
-    for (int i = 8; i >= 0; --i) p = __fma_rn(p, z, kCosPiD[i]);
+    for (int i = 7; i >= 0; --i) p = __fma_rn(p, z, kCosPiD[i]);
     return flip(p, odd);
   }
   static __device__ __forceinline__ double sin_(double w) {

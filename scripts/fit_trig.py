@@ -42,7 +42,7 @@ def err(f, c, zmax, scale, n=4000):
 cosf_ = lambda z: mp.cos(mp.pi * mp.sqrt(z))                          # noqa: E731
 sinq_ = lambda z: (mp.sin(mp.sqrt(z)) / mp.sqrt(z)) if z > 0 else mp.mpf(1)  # noqa: E731
 for name, f, zmax, deg, single, scale in [
-    ("COS_PI_D", cosf_, mp.mpf(1) / 4, 9, False, lambda z: 1),
+    ("COS_PI_D", cosf_, mp.mpf(1) / 4, 8, False, lambda z: 1),
     ("COS_PI_F", cosf_, mp.mpf(1) / 4, 5, True, lambda z: 1),
     ("SIN_Q_D", sinq_, (mp.pi / 2) ** 2, 9, False, lambda z: mp.sqrt(z)),
     ("SIN_Q_F", sinq_, (mp.pi / 2) ** 2, 5, True, lambda z: mp.sqrt(z)),
