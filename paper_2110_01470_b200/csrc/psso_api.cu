@@ -740,7 +740,9 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
         // | per-warp smem rows (f3, f7, f8)
         const int nw = PSSO_CHAIN_NT / 32;
         const bool smem_fn = cfg->fn_id == 3 || cfg->fn_id == 7 || cfg->fn_id == 8;
-        c->LF.off_red = (int)align16((size_t)D * es);
+        // (gbest padded to 8M entries: rows shorter than 8M read, and discard,
+        // gbest past D in the branch-free select)
+        c->LF.off_red = (int)align16((size_t)8 * M * es);
         c->LF.off_bar = (int)align16((size_t)c->LF.off_red + 128 + 64 * M);
         c->LF.off_xs = (int)((c->LF.off_bar + 8 * nw + 127) & ~127);
         c->LF.off_scr = (int)align16((size_t)c->LF.off_xs +

@@ -1390,6 +1390,7 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, PSSO_CHAIN_MINB)
           pv[m] = (T)0;
         }
       }
+      __syncwarp();  // clamped last-row loads precede the valid segment's stores
     } else {
 #pragma unroll
       for (int m = 0; m < M; ++m) pv[m] = (T)0;

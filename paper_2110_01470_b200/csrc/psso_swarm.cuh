@@ -368,6 +368,9 @@ __global__ void __launch_bounds__(PSSO_SWARM_NT, 1)
         x[m] = j < D ? xl[j] : (T)0;
         pv[m] = j < D ? pl[j] : (T)0;
       }
+      // a segment past the last row reads the (clamped) last row, which the
+      // valid segment of the same warp rewrites below: loads before stores
+      __syncwarp();
       chain_step<T, FN, RNG, M, false, false, RES>(p, ev, gb, xg, scr, r - r0, rv, x, pv, pf_row,
                                                    best_f, best_i, best_new);
     }

@@ -1,0 +1,35 @@
+"""Small runs of every kernel family, for compute-sanitizer (memcheck / racecheck / synccheck).
+
+    compute-sanitizer --tool memcheck python scripts/sanitize_run.py
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2110_01470_b200 as psso  # noqa: E402
+from paper_2110_01470_b200 import _lib  # noqa: E402
+from paper_2110_01470_b200.engine import DeviceEngine  # noqa: E402
+
+CASES = [("f5", 1 << 14, 128, 3), ("f4", 4099, 64, 3), ("f6", 66, 4096, 2), ("f2", 130, 1024, 2),
+         ("f5", 300, 300, 2), ("f9", 200, 301, 2), ("f5", 1024, 100, 4), ("f7", 256, 100, 3),
+         ("f1", 100, 30, 5)]
+torch.cuda.set_device(0)
+L = _lib.load()
+for fid, n, d, it in CASES:
+    fn = psso.make_function(fid, d)
+    p = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=fn.var_min, var_max=fn.var_max,
+                       nsol=n, nvar=d, niter=it)
+    eng = DeviceEngine(p, fn, 1, keep_sol_f=True)
+    name = L.psso_kernel_name(eng.ctx).decode()
+    eng.initialize()
+    eng.run(0, it)
+    eng.check()
+    torch.cuda.synchronize()
+    eng.close()
+    print("ok", name, flush=True)
+recs = psso.run_parallel_batch(psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=-5.12, var_max=5.12,
+                                              nsol=64, nvar=16, niter=5),
+                               psso.make_function("f5", 16), [1, 2, 3])
+print("ok batch", len(recs), flush=True)
