@@ -12,7 +12,8 @@ import paper_2110_01470_b200 as psso  # noqa: E402
 from paper_2110_01470_b200 import _lib  # noqa: E402
 from paper_2110_01470_b200.engine import DeviceEngine  # noqa: E402
 
-CASES = [("f5", 1 << 14, 128, 3), ("f4", 4099, 64, 3), ("f6", 66, 4096, 2), ("f2", 130, 1024, 2),
+CASES = [("f5", 1 << 16, 128, 2), ("f4", 70000, 64, 2), ("f5", 50000, 100, 2),  # k_chain
+         ("f5", 1 << 14, 128, 3), ("f4", 4099, 64, 3), ("f6", 66, 4096, 2), ("f2", 130, 1024, 2),
          ("f5", 300, 300, 2), ("f9", 200, 301, 2), ("f5", 1024, 100, 4), ("f7", 256, 100, 3),
          ("f1", 100, 30, 5)]
 torch.cuda.set_device(0)
