@@ -592,3 +592,46 @@ def test_dispatch_paths_against_oracle(fid, nsol, nvar, box, kernel):
     assert np.array_equal(sw.sol, osw.sol) and np.array_equal(sw.pbests, osw.pbests)
     assert np.array_equal(sw.gbest, osw.gbest)
     assert _close(sw.p_f, osw.p_f, fid) and _close(traj, otraj, fid)
+
+
+# ------------------------------------------ reference test-strategy gaps ----
+
+def test_rng_uniformity_seed_masking_and_key_sensitivity():
+    """reference test_rng.py:23-53 -- chi^2 per substream, 64-bit seed masking, key sensitivity."""
+    n_i, n_j = 1000, 1000  # 10^6 draws per substream
+    i = np.arange(n_i, dtype=np.uint64)[:, None]
+    j = np.arange(n_j, dtype=np.uint64)[None, :]
+    rng = psso.RngStream(12345)
+    for stream in psso.SubStream:
+        u = rng.uniform(stream, 3, i, j).ravel()
+        assert u.min() >= 0.0 and u.max() < 1.0
+        counts = np.bincount(np.minimum((u * 100).astype(int), 99), minlength=100)
+        chi2 = float(((counts - u.size / 100) ** 2 / (u.size / 100)).sum())
+        assert chi2 < 160.0, (stream, chi2)  # 99 dof: p ~ 1e-4
+    a = psso.RngStream(7).uniform(psso.SubStream.BRANCH, 1, i[:10], j[:, :10])
+    b = psso.RngStream(7 + (1 << 64)).uniform(psso.SubStream.BRANCH, 1, i[:10], j[:, :10])
+    assert np.array_equal(a, b)  # seeds are masked to 64 bits
+    for other in (psso.RngStream(8).uniform(psso.SubStream.BRANCH, 1, i[:10], j[:, :10]),
+                  psso.RngStream(7).uniform(psso.SubStream.BRANCH, 2, i[:10], j[:, :10]),
+                  psso.RngStream(7).uniform(psso.SubStream.FRESH, 1, i[:10], j[:, :10])):
+        assert np.mean(a == other) < 0.01  # every key component changes the draws
+
+
+def test_branch_law_on_a_million_draws():
+    """Acceptance C3 (reference test_acceptance.py:101-113): branch frequencies follow the thresholds."""
+    cw, cp, cg = 0.3, 0.6, 0.8
+    u = psso.RngStream(0).uniform(psso.SubStream.BRANCH, 5, np.arange(1000, dtype=np.uint64)[:, None],
+                                  np.arange(1000, dtype=np.uint64)[None, :]).ravel()
+    freq = np.array([np.mean(u < cw), np.mean((u >= cw) & (u < cp)), np.mean((u >= cp) & (u < cg)),
+                     np.mean(u >= cg)])
+    assert np.allclose(freq, [0.3, 0.3, 0.2, 0.2], atol=0.003), freq
+
+
+@pytest.mark.parametrize("fid,nsol,nvar", [("f1", 100, 30), ("f5", 1 << 16, 128)])
+def test_shorter_run_is_a_prefix(fid, nsol, nvar):
+    """reference test_core.py:186-191: the keyed RNG makes a shorter run an exact prefix."""
+    fn = _fn(fid, nvar)
+    short = psso.run_parallel(_params(fn, nsol, 20), fn, 4)
+    long_ = psso.run_parallel(_params(fn, nsol, 45), fn, 4)
+    assert np.array_equal(long_.trajectory[:20], short.trajectory)
+    assert np.all(np.diff(long_.trajectory) <= 0)  # g_f is monotone (parallel.py:209)
