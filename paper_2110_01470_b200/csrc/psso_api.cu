@@ -825,7 +825,11 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
         delete c;
         return cuda_fail(nullptr, e, "psso_create swarm kernel");
       }
-      if (sp.fn) {
+      // measured (scripts/swarm_crossover.py): the whole-run kernel beats the
+      // graph-replayed streaming kernels only in its cluster form with at most
+      // one row group per warp (C1, C2); the global-exchange forms are slower
+      // and serve batches of many swarms (psso_solve_batch) only
+      if (sp.fn && sp.cl && sp.gpc <= PSSO_SWARM_NT / 32) {
         c->swarm_fn = sp.fn;
         c->swarm = sp;
       }
@@ -1305,7 +1309,7 @@ int psso_solve_batch(const psso_config* cfg, const uint64_t* seeds, int32_t nsee
   if (cfg->row_lo != 0 || cfg->row_hi != cfg->nsol) return fail(nullptr, PSSO_E_INVALID, "psso_solve_batch runs whole swarms");
   psso_ctx* c = nullptr;
   if ((rc = psso_create(cfg, &c)) != PSSO_OK) return rc;
-  if (!c->swarm_fn) {
+  if (!c->chain || cfg->nsol * cfg->nvar > PSSO_SWARM_MAX_ELEMS) {
     psso_destroy(c);
     return fail(nullptr, PSSO_E_UNSUPPORTED, "batched runs need nvar <= 128 and nsol*nvar <= 2^22 (whole-run kernel)");
   }

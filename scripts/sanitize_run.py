@@ -34,3 +34,7 @@ recs = psso.run_parallel_batch(psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=-5
                                               nsol=64, nvar=16, niter=5),
                                psso.make_function("f5", 16), [1, 2, 3])
 print("ok batch", len(recs), flush=True)
+recs = psso.run_parallel_batch(psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=-5.12, var_max=5.12,
+                                              nsol=4096, nvar=128, niter=3),
+                               psso.make_function("f5", 128), [1, 2, 3])
+print("ok batch (global-memory exchange)", len(recs), flush=True)

@@ -526,7 +526,8 @@ def test_whole_run_kernel_other_modes(dtype, rng, monkeypatch):
     ("f1", 100, 30, 200, 5),    # C1 shape, co-resident swarms with a swarm barrier each
     ("f5", 1024, 100, 30, 3),   # C2 shape
     ("f7", 256, 100, 20, 4),
-    ("f4", 60, 16, 50, 300),    # more swarms than co-resident CTAs: one CTA per swarm
+    ("f4", 60, 16, 50, 300),    # 300 clusters of 2 CTAs
+    ("f5", 4096, 128, 10, 3),   # too big for one cluster: global-memory exchange, rows in HBM
 ])
 def test_batch_runs_equal_single_runs(fid, nsol, nvar, niter, nseeds):
     fn = _fn(fid, nvar)
