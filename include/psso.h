@@ -106,9 +106,10 @@ int psso_init(psso_ctx* ctx);
 int psso_step(psso_ctx* ctx, int64_t t);
 
 /* replaces: the whole loop `for t in range(t0, t0+niter)` (parallel.py:192-212).
- * Asynchronous.  Swarms of up to 2^22 elements run all iterations in ONE
- * persistent launch (k_swarm, swarm barrier per iteration); larger swarms
- * replay the fused + gBest kernel pair from a captured CUDA graph. */
+ * Asynchronous.  Small swarms that fit one thread-block cluster (C1, C2
+ * shapes) run all iterations in ONE persistent launch (k_swarm: cluster
+ * barrier + DSMEM gBest exchange per iteration); larger swarms replay the
+ * fused + gBest kernel pair from a captured CUDA graph. */
 int psso_run(psso_ctx* ctx, int64_t t0, int64_t niter);
 
 /* Name of the iteration kernel psso_run uses for this configuration
