@@ -137,6 +137,32 @@ int psso_init_local(psso_ctx* ctx, void* cand);
 int psso_step_local(psso_ctx* ctx, int64_t t, void* cand);
 int psso_apply_candidates(psso_ctx* ctx, int64_t t, const void* cands, int32_t ncand, int32_t is_init);
 
+/* Device-initiated gBest exchange (replaces the NCCL all-gather of the
+ * records; SURVEY §8 f #3).  Every rank owns an exchange buffer of
+ * psso_p2p_buffer_bytes(cfg, R) bytes ([2][R] epoch flags, [2][R] candidate
+ * records: double-buffered by epoch parity, since a rank may run one exchange ahead),
+ * allocated with psso_p2p_alloc; peers map it through psso_p2p_handle /
+ * psso_p2p_open (CUDA IPC over NVLink P2P).  Per iteration, after
+ * psso_step_local / psso_init_local wrote the local record `cand`:
+ *   psso_publish_p2p: stores `cand` into slot `rank` of every rank's buffer
+ *     (`peer_bufs` = DEVICE array of R buffer pointers, own included) and
+ *     raises this rank's flag in each buffer to `epoch` (system-scope release);
+ *   psso_apply_p2p: waits until the R flags of this rank's buffer reached
+ *     `epoch` (system-scope acquire), then applies the selection exactly like
+ *     psso_apply_candidates.
+ * `epoch` must increase by at least 1 per exchange (buffers start at 0).
+ * No host synchronization and no collective library on the path. */
+int64_t psso_p2p_buffer_bytes(const psso_config* cfg, int32_t nranks);
+int psso_p2p_alloc(int64_t bytes, void** dev_ptr);
+int psso_p2p_free(void* dev_ptr);
+int psso_p2p_handle(void* dev_ptr, void* handle /* 64 bytes (cudaIpcMemHandle_t) */);
+int psso_p2p_open(const void* handle, void** dev_ptr);
+int psso_p2p_close(void* dev_ptr);
+int psso_publish_p2p(psso_ctx* ctx, const void* cand, void* const* peer_bufs, int32_t nranks,
+                     int32_t rank, uint64_t epoch);
+int psso_apply_p2p(psso_ctx* ctx, int64_t t, const void* my_buf, int32_t nranks, uint64_t epoch,
+                   int32_t is_init);
+
 /* Synchronizes the stream and reports the first non-finite fitness seen so
  * far as (iteration, particle); iteration -1 = initialization.  Returns
  * PSSO_E_NONFINITE if there was one (core.py:190-193 semantics). */

@@ -32,7 +32,9 @@ EXPORTS = (
     "psso_update_pbests", "psso_update_gbest", "psso_candidate_bytes", "psso_init_local",
     "psso_step_local", "psso_apply_candidates", "psso_check", "psso_launch_count",
     "psso_rng_uniform", "psso_eval_rows", "psso_solve", "psso_profile", "psso_profile_read",
-    "psso_kernel_name", "psso_solve_batch",
+    "psso_kernel_name", "psso_solve_batch", "psso_p2p_buffer_bytes", "psso_p2p_alloc",
+    "psso_p2p_free", "psso_p2p_handle", "psso_p2p_open", "psso_p2p_close", "psso_publish_p2p",
+    "psso_apply_p2p",
 )
 
 
@@ -120,6 +122,15 @@ def load():
     L.psso_solve_batch.argtypes = [cfgp, vp, i32, i64, vp, vp, vp, ctypes.POINTER(dbl)]
     L.psso_kernel_name.argtypes = [vp]
     L.psso_kernel_name.restype = ctypes.c_char_p
+    L.psso_p2p_buffer_bytes.argtypes = [cfgp, i32]
+    L.psso_p2p_buffer_bytes.restype = i64
+    L.psso_p2p_alloc.argtypes = [i64, ctypes.POINTER(vp)]
+    L.psso_p2p_free.argtypes = [vp]
+    L.psso_p2p_handle.argtypes = [vp, vp]
+    L.psso_p2p_open.argtypes = [vp, ctypes.POINTER(vp)]
+    L.psso_p2p_close.argtypes = [vp]
+    L.psso_publish_p2p.argtypes = [vp, vp, vp, i32, i32, u64]
+    L.psso_apply_p2p.argtypes = [vp, i64, vp, i32, u64, i32]
     for name in EXPORTS:
         if not hasattr(L, name):
             raise RuntimeError(f"{LIB_PATH} does not export {name}")

@@ -283,6 +283,82 @@ __global__ void __launch_bounds__(GB_THREADS) k_apply(const __grid_constant__ Gb
 }
 
 // per-CTA argmin of p_f over local rows (update_gbest_phase, parallel.py:138-144)
+// Device-initiated gBest exchange (SURVEY §8 f #3).  Exchange buffer of a
+// rank: [2][R] epoch flags (u64, padded to 16 B), [2][R] candidate records,
+// both indexed by epoch parity.
+// k_publish stores this rank's record into slot `rank` of EVERY rank's buffer
+// (peer pointers: CUDA-IPC / NVLink P2P mappings, or plain pointers for
+// virtual ranks on one GPU), then raises its flag in each buffer with a
+// system-scope release; k_apply_p2p waits for all R flags of its own buffer
+// (system-scope acquire) and applies the selection exactly like k_apply.
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(GB_THREADS) k_publish(const unsigned char* cand,
+                                                        unsigned char* const* bufs, int R, int rank,
+                                                        unsigned long long epoch, int64_t rec_bytes,
+                                                        int64_t flag_bytes) {
+  const uint64_t* src = reinterpret_cast<const uint64_t*>(cand);
+  const int64_t words = rec_bytes / 8;
+  const int slot = (int)(epoch & 1) * R + rank;  // records double-buffered by epoch parity
+  for (int q = 0; q < R; ++q) {
+    uint64_t* dst = reinterpret_cast<uint64_t*>(bufs[q] + flag_bytes + (int64_t)slot * rec_bytes);
+    for (int64_t w = threadIdx.x; w < words; w += blockDim.x) dst[w] = src[w];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int q = 0; q < R; ++q)
+      st_release_sys_u64(reinterpret_cast<unsigned long long*>(bufs[q]) + slot, epoch);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(GB_THREADS) k_apply_p2p(const __grid_constant__ GbParams g,
+                                                          const unsigned char* buf, int R,
+                                                          unsigned long long epoch, int64_t rec_bytes,
+                                                          int64_t flag_bytes) {
+  __shared__ int winner;
+  __shared__ int take_s;
+  // a rank can publish epoch e+1 before a slower rank applied epoch e, never
+  // e+2 (that needs the slower rank's e+1 record): parity buffers suffice
+  const int par = (int)(epoch & 1);
+  const unsigned char* recs = buf + flag_bytes + (int64_t)par * R * rec_bytes;
+  if (threadIdx.x == 0) {
+    const unsigned long long* flags = reinterpret_cast<const unsigned long long*>(buf) + par * R;
+    for (int q = 0; q < R; ++q)
+      while (ld_acquire_sys_u64(flags + q) < epoch) __nanosleep(32);
+    double bf = CUDART_INF;
+    int64_t bi = INT64_MAX;
+    int w = 0;
+    for (int k = 0; k < R; ++k) {
+      const unsigned char* r = recs + k * rec_bytes;
+      const double f = __ldcg(reinterpret_cast<const double*>(r));
+      const int64_t i = __ldcg(reinterpret_cast<const long long*>(r + 8));
+      if (lex_less(f, i, bf, bi)) { bf = f; bi = i; w = k; }
+    }
+    const double inc = *g.g_f;
+    take_s = bi != INT64_MAX && (g.is_init || bf <= inc);  // parallel.py:209
+    winner = w;
+    const double gf = take_s ? bf : inc;
+    if (take_s) *g.g_f = gf;
+    if (g.traj && g.t_arg >= 0) g.traj[g.t_arg] = gf;
+    __threadfence_block();
+  }
+  __syncthreads();
+  if (take_s) {
+    const T* src = reinterpret_cast<const T*>(recs + winner * rec_bytes + 16);
+    T* dst = reinterpret_cast<T*>(g.gbest);
+    for (int j = threadIdx.x; j < g.D; j += blockDim.x) dst[j] = __ldcg(src + j);
+  }
+}
+
 __global__ void k_argmin(const double* f, int64_t n, int64_t row_lo, double* slot_f,
                          int64_t* slot_i) {
   __shared__ double sf[32];
@@ -1143,6 +1219,72 @@ int psso_apply_candidates(psso_ctx* c, int64_t t, const void* cands, int32_t nca
     k_apply<double><<<1, GB_THREADS, 0, c->stream>>>(g, (const unsigned char*)cands, rb, ncand);
   else
     k_apply<float><<<1, GB_THREADS, 0, c->stream>>>(g, (const unsigned char*)cands, rb, ncand);
+  c->launches++;
+  CK(c, cudaGetLastError());
+  return PSSO_OK;
+}
+
+int64_t psso_p2p_buffer_bytes(const psso_config* cfg, int32_t nranks) {
+  if (!cfg || nranks < 1) return 0;
+  return (int64_t)align16((size_t)nranks * 16) + 2 * (int64_t)nranks * psso_candidate_bytes(cfg);
+}
+
+int psso_p2p_alloc(int64_t bytes, void** dev_ptr) {
+  if (!dev_ptr || bytes <= 0) return fail(nullptr, PSSO_E_INVALID, "bad p2p buffer size");
+  cudaError_t e = cudaMalloc(dev_ptr, (size_t)bytes);
+  if (e == cudaSuccess) e = cudaMemset(*dev_ptr, 0, (size_t)bytes);
+  return e == cudaSuccess ? PSSO_OK : cuda_fail(nullptr, e, "psso_p2p_alloc");
+}
+
+int psso_p2p_free(void* dev_ptr) {
+  cudaError_t e = cudaFree(dev_ptr);
+  return e == cudaSuccess ? PSSO_OK : cuda_fail(nullptr, e, "psso_p2p_free");
+}
+
+int psso_p2p_handle(void* dev_ptr, void* handle) {
+  if (!dev_ptr || !handle) return fail(nullptr, PSSO_E_INVALID, "null pointer");
+  cudaError_t e = cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(handle), dev_ptr);
+  return e == cudaSuccess ? PSSO_OK : cuda_fail(nullptr, e, "psso_p2p_handle");
+}
+
+int psso_p2p_open(const void* handle, void** dev_ptr) {
+  if (!dev_ptr || !handle) return fail(nullptr, PSSO_E_INVALID, "null pointer");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof h);
+  cudaError_t e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  return e == cudaSuccess ? PSSO_OK : cuda_fail(nullptr, e, "psso_p2p_open");
+}
+
+int psso_p2p_close(void* dev_ptr) {
+  cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+  return e == cudaSuccess ? PSSO_OK : cuda_fail(nullptr, e, "psso_p2p_close");
+}
+
+int psso_publish_p2p(psso_ctx* c, const void* cand, void* const* peer_bufs, int32_t nranks,
+                     int32_t rank, uint64_t epoch) {
+  if (int rc = need_bound(c)) return rc;
+  if (!cand || !peer_bufs || nranks < 1 || rank < 0 || rank >= nranks || epoch == 0)
+    return fail(c, PSSO_E_INVALID, "bad p2p publish arguments");
+  const int64_t rb = psso_candidate_bytes(&c->cfg);
+  k_publish<<<1, GB_THREADS, 0, c->stream>>>((const unsigned char*)cand, (unsigned char* const*)peer_bufs,
+                                             nranks, rank, epoch, rb, (int64_t)align16((size_t)nranks * 16));
+  c->launches++;
+  CK(c, cudaGetLastError());
+  return PSSO_OK;
+}
+
+int psso_apply_p2p(psso_ctx* c, int64_t t, const void* my_buf, int32_t nranks, uint64_t epoch,
+                   int32_t is_init) {
+  if (int rc = need_bound(c)) return rc;
+  if (!my_buf || nranks < 1 || epoch == 0) return fail(c, PSSO_E_INVALID, "bad p2p apply arguments");
+  GbParams g = gb_params(c, t, nullptr, is_init, 0);
+  if (is_init) g.traj = nullptr;
+  g.t_arg = is_init ? -1 : t;
+  const int64_t rb = psso_candidate_bytes(&c->cfg), fb = (int64_t)align16((size_t)nranks * 16);
+  if (c->cfg.dtype == PSSO_F64)
+    k_apply_p2p<double><<<1, GB_THREADS, 0, c->stream>>>(g, (const unsigned char*)my_buf, nranks, epoch, rb, fb);
+  else
+    k_apply_p2p<float><<<1, GB_THREADS, 0, c->stream>>>(g, (const unsigned char*)my_buf, nranks, epoch, rb, fb);
   c->launches++;
   CK(c, cudaGetLastError());
   return PSSO_OK;

@@ -158,6 +158,15 @@ class DeviceEngine:
     def apply(self, t, cands, ncand, is_init=False):
         self._call("psso_apply_candidates", int(t), cands.data_ptr(), int(ncand), int(bool(is_init)))
 
+    def publish_p2p(self, cand, peer_table, nranks, rank, epoch):
+        """This shard's record into slot ``rank`` of every rank's exchange buffer (psso_publish_p2p)."""
+        self._call("psso_publish_p2p", cand.data_ptr(), peer_table.data_ptr(), int(nranks), int(rank),
+                   int(epoch))
+
+    def apply_p2p(self, t, my_buf, nranks, epoch, is_init=False):
+        """Wait for the epoch's records in this shard's buffer, then select (psso_apply_p2p)."""
+        self._call("psso_apply_p2p", int(t), int(my_buf), int(nranks), int(epoch), int(bool(is_init)))
+
     # -- host <-> device -------------------------------------------------------
     def to_host(self) -> Swarm:
         self.stream.synchronize()

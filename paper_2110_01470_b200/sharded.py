@@ -18,6 +18,13 @@ Exchanges:
                                 shards on one GPU); gather = concatenation.
   * ``ProcessGroupExchange`` -- one shard per process over torch.distributed
                                 (NCCL over NVLink on B200; gloo on CPU tests).
+  * ``P2PExchange``          -- device-initiated (SURVEY §8 f #3): each shard's
+                                kernel stores its record straight into every
+                                shard's exchange buffer (CUDA-IPC mappings over
+                                NVLink P2P across processes; plain pointers for
+                                virtual shards) and raises an epoch flag; each
+                                shard's apply kernel waits on the flags.  No
+                                host synchronization, no collective library.
 """
 
 from __future__ import annotations
@@ -31,6 +38,7 @@ __all__ = [
     "partition",
     "LocalExchange",
     "ProcessGroupExchange",
+    "P2PExchange",
     "ShardedDriver",
     "run_virtual_shards",
     "run_parallel_distributed",
@@ -73,6 +81,88 @@ class ProcessGroupExchange:
         return out
 
 
+class P2PExchange:
+    """Device-initiated record exchange through per-rank exchange buffers (psso_publish_p2p).
+
+    ``engines``: the shards this process owns.  ``distributed=False``: they
+    are all the ranks (virtual shards, rank = position).  ``distributed=True``:
+    this process owns exactly one shard (rank = rank in the torch.distributed
+    ``group``, None = default group) and the buffers of the other ranks are
+    mapped through CUDA IPC handles exchanged over the group.  Call
+    :meth:`close` to unmap and free.
+    """
+
+    HANDLE_BYTES = 64
+
+    def __init__(self, engines, group=None, distributed=False):
+        import ctypes
+
+        import numpy as np
+        import torch
+
+        from . import _lib
+
+        self.L = _lib.load()
+        self.engines = list(engines)
+        self.group = group
+        self.epoch = 0
+        first = self.engines[0]
+        self.distributed = bool(distributed)
+        if not self.distributed:
+            self.world, self.ranks = len(self.engines), list(range(len(self.engines)))
+        else:
+            import torch.distributed as dist
+
+            if len(self.engines) != 1:
+                raise ValueError("a process-group P2P exchange drives exactly one shard per process")
+            self.world, self.ranks = dist.get_world_size(group), [dist.get_rank(group)]
+        nbytes = int(self.L.psso_p2p_buffer_bytes(ctypes.byref(first.cfg), self.world))
+        self.own = []
+        for _ in self.engines:
+            ptr = ctypes.c_void_p()
+            _lib.check(self.L.psso_p2p_alloc(nbytes, ctypes.byref(ptr)))
+            self.own.append(ptr.value)
+        self.opened = []
+        if not self.distributed:
+            table = self.own
+        else:
+            import torch.distributed as dist
+
+            h = (ctypes.c_ubyte * self.HANDLE_BYTES)()
+            _lib.check(self.L.psso_p2p_handle(ctypes.c_void_p(self.own[0]), h))
+            handles = [None] * self.world
+            dist.all_gather_object(handles, bytes(h), group=group)
+            table = []
+            for r, hb in enumerate(handles):
+                if r == self.ranks[0]:
+                    table.append(self.own[0])
+                    continue
+                ptr = ctypes.c_void_p()
+                buf = (ctypes.c_ubyte * self.HANDLE_BYTES).from_buffer_copy(hb)
+                _lib.check(self.L.psso_p2p_open(buf, ctypes.byref(ptr)))
+                self.opened.append(ptr.value)
+                table.append(ptr.value)
+        self.table = torch.tensor(np.array(table, dtype=np.uint64).view(np.int64), device=first.device)
+
+    def exchange_and_apply(self, engines, cands, t: int, is_init: bool):
+        self.epoch += 1
+        for e, c, r in zip(engines, cands, self.ranks):
+            e.publish_p2p(c, self.table, self.world, r, self.epoch)
+        for e, buf in zip(engines, self.own):
+            e.apply_p2p(t, buf, self.world, self.epoch, is_init)
+
+    def close(self):
+        import ctypes
+
+        for e in self.engines:
+            e.synchronize()
+        for p in self.opened:
+            self.L.psso_p2p_close(ctypes.c_void_p(p))
+        for p in self.own:
+            self.L.psso_p2p_free(ctypes.c_void_p(p))
+        self.opened, self.own = [], []
+
+
 class ShardedDriver:
     """Drives shard engines through init / iterations around the exchange.
 
@@ -89,6 +179,9 @@ class ShardedDriver:
         self.cands = [e.new_candidate() for e in self.engines]
 
     def _exchange_and_apply(self, t: int, is_init: bool):
+        if hasattr(self.exchange, "exchange_and_apply"):  # device-initiated exchange
+            self.exchange.exchange_and_apply(self.engines, self.cands, t, is_init)
+            return None
         gathered = self.exchange.gather(self.cands)
         for e in self.engines:
             e.apply(t, gathered, self.ncand, is_init)
@@ -124,8 +217,12 @@ def _record(params, f, seed, best, wall, traj, best_position) -> RunRecord:
 
 
 def run_virtual_shards(params: SsoParams, f, seed: int, shards: int, *, dtype="float64",
-                       rng="reference", device=None) -> RunRecord:
-    """``shards`` contiguous shards on one GPU with the candidate exchange (tests sharding)."""
+                       rng="reference", device=None, exchange: str = "gather") -> RunRecord:
+    """``shards`` contiguous shards on one GPU with the candidate exchange (tests sharding).
+
+    ``exchange``: "gather" (concatenate records, like the NCCL all-gather) or
+    "p2p" (the device-initiated exchange through per-shard buffers).
+    """
     import torch
 
     from .engine import DeviceEngine
@@ -138,8 +235,9 @@ def run_virtual_shards(params: SsoParams, f, seed: int, shards: int, *, dtype="f
                      device=device, stream=first.stream)
         for lo, hi in ranges[1:]
     ]
+    ex = P2PExchange(engines) if exchange == "p2p" else LocalExchange()
     try:
-        drv = ShardedDriver(engines, LocalExchange(), len(engines))
+        drv = ShardedDriver(engines, ex, len(engines))
         with torch.cuda.stream(first.stream):
             drv.initialize()
             start = torch.cuda.Event(enable_timing=True)
@@ -152,30 +250,36 @@ def run_virtual_shards(params: SsoParams, f, seed: int, shards: int, *, dtype="f
         return _record(params, f, seed, float(first.g_f.cpu()[0]), wall, first.traj.cpu().numpy(),
                        first.gbest.to(torch.float64).cpu().numpy())
     finally:
+        if exchange == "p2p":
+            ex.close()
         for e in engines:
             e.close()
 
 
 def run_parallel_distributed(params: SsoParams, f, seed: int, *, group=None, dtype="float64",
-                             rng="reference") -> RunRecord:
+                             rng="reference", exchange: str = "collective") -> RunRecord:
     """One shard per torch.distributed rank (one process per GPU, NCCL over NVLink).
 
     Every rank returns the same RunRecord.  ``wall_time_s`` is this rank's
     loop time; callers wanting the job time take the max over ranks.
+    ``exchange``: "collective" (all-gather over the process group) or "p2p"
+    (device-initiated stores into CUDA-IPC-mapped peer buffers; the group is
+    only used once, to exchange the IPC handles).
     """
     import torch
     import torch.distributed as dist
 
     from .engine import DeviceEngine
 
-    ex = ProcessGroupExchange(group)
-    ranges = partition(params.nsol, ex.world)
-    if len(ranges) != ex.world:
-        raise ValueError(f"nsol={params.nsol} cannot give every one of {ex.world} ranks a particle")
-    lo, hi = ranges[ex.rank]
+    pg = ProcessGroupExchange(group)
+    ranges = partition(params.nsol, pg.world)
+    if len(ranges) != pg.world:
+        raise ValueError(f"nsol={params.nsol} cannot give every one of {pg.world} ranks a particle")
+    lo, hi = ranges[pg.rank]
     eng = DeviceEngine(params, f, seed, dtype=dtype, rng=rng, row_lo=lo, row_hi=hi)
+    ex = P2PExchange([eng], group=group, distributed=True) if exchange == "p2p" else pg
     try:
-        drv = ShardedDriver([eng], ex, ex.world)
+        drv = ShardedDriver([eng], ex, pg.world)
         with torch.cuda.stream(eng.stream):
             drv.initialize()
             dist.barrier(group)
@@ -189,4 +293,7 @@ def run_parallel_distributed(params: SsoParams, f, seed: int, *, group=None, dty
         return _record(params, f, seed, float(eng.g_f.cpu()[0]), wall, eng.traj.cpu().numpy(),
                        eng.gbest.to(torch.float64).cpu().numpy())
     finally:
+        if exchange == "p2p":
+            dist.barrier(group)  # every rank done reading before buffers are unmapped
+            ex.close()
         eng.close()

@@ -3,11 +3,13 @@
     torchrun --nproc-per-node 1 --master-addr 127.0.0.1 scripts/exchange_overhead.py
 
 For each per-rank shard shape, times K iterations of (a) the plain
-single-context loop and (b) the sharded loop -- psso_step_local, NCCL
-all_gather of the candidate records, psso_apply_candidates -- with world size
-1.  (b) - (a) is the fixed per-iteration cost of the exchange path that an
-N-GPU run pays on top of its shard's compute (the NVLink transfer of
-R * (16 + D * 8) bytes is negligible next to it).
+single-context loop, (b) the sharded loop -- psso_step_local, NCCL
+all_gather of the candidate records, psso_apply_candidates -- and (c) the
+sharded loop with the device-initiated P2P exchange (psso_publish_p2p /
+psso_apply_p2p), with world size 1.  (b) - (a) and (c) - (a) are the fixed
+per-iteration costs of the exchange paths that an N-GPU run pays on top of
+its shard's compute (the NVLink transfer of R * (16 + D * 8) bytes is
+negligible next to them).
 """
 import os
 import sys
@@ -19,7 +21,7 @@ import torch.distributed as dist
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2110_01470_b200 as psso  # noqa: E402
 from paper_2110_01470_b200.engine import DeviceEngine  # noqa: E402
-from paper_2110_01470_b200.sharded import ProcessGroupExchange, ShardedDriver  # noqa: E402
+from paper_2110_01470_b200.sharded import P2PExchange, ProcessGroupExchange, ShardedDriver  # noqa: E402
 
 torch.cuda.set_device(0)
 dist.init_process_group("nccl", device_id=torch.device("cuda", 0))
@@ -32,9 +34,14 @@ for fid, rows, D, label in (("f4", 1 << 21, 64, "C4 share of 8 GPUs (2^24/8 rows
     p = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=fn.var_min, var_max=fn.var_max,
                        nsol=rows, nvar=D, niter=K + 10)
     res = {}
-    for mode in ("plain", "sharded"):
+    for mode in ("plain", "sharded", "p2p"):
         eng = DeviceEngine(p, fn, 0, keep_sol_f=False, row_lo=0, row_hi=rows)
-        drv = ShardedDriver([eng], ProcessGroupExchange(), 1) if mode == "sharded" else None
+        ex = None
+        if mode == "sharded":
+            ex = ProcessGroupExchange()
+        elif mode == "p2p":
+            ex = P2PExchange([eng], distributed=True)
+        drv = ShardedDriver([eng], ex, 1) if ex is not None else None
         with torch.cuda.stream(eng.stream):
             (drv.initialize() if drv else eng.initialize())
             (drv.run(0, 5) if drv else eng.run(0, 5))
@@ -45,8 +52,11 @@ for fid, rows, D, label in (("f4", 1 << 21, 64, "C4 share of 8 GPUs (2^24/8 rows
             b.record(eng.stream)
         torch.cuda.synchronize()
         res[mode] = a.elapsed_time(b) / K
+        if mode == "p2p":
+            ex.close()
         eng.close()
     print(json.dumps({"shape": label, "rows": rows, "nvar": D,
-                      "plain_ms": res["plain"], "sharded_ms": res["sharded"],
-                      "exchange_overhead_us": 1e3 * (res["sharded"] - res["plain"])}), flush=True)
+                      "plain_ms": res["plain"], "sharded_ms": res["sharded"], "p2p_ms": res["p2p"],
+                      "exchange_overhead_us": 1e3 * (res["sharded"] - res["plain"]),
+                      "p2p_overhead_us": 1e3 * (res["p2p"] - res["plain"])}), flush=True)
 dist.destroy_process_group()

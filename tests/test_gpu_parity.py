@@ -636,3 +636,63 @@ def test_shorter_run_is_a_prefix(fid, nsol, nvar):
     long_ = psso.run_parallel(_params(fn, nsol, 45), fn, 4)
     assert np.array_equal(long_.trajectory[:20], short.trajectory)
     assert np.all(np.diff(long_.trajectory) <= 0)  # g_f is monotone (parallel.py:209)
+
+
+# ------------------------------- device-initiated gBest exchange (P2P) ----
+
+@pytest.mark.parametrize("shards", [2, 3, 7])
+def test_p2p_exchange_virtual_shards_bitwise(shards):
+    """Records stored straight into every shard's buffer + epoch flags == one shard."""
+    fn = _fn("f5", 64)
+    p = _params(fn, 4096 + 5, 30)
+    one = psso.run_parallel(p, fn, 9)
+    from paper_2110_01470_b200.sharded import run_virtual_shards
+
+    rec = run_virtual_shards(p, fn, 9, shards, exchange="p2p")
+    assert np.array_equal(rec.trajectory, one.trajectory)
+    assert np.array_equal(rec.best_position, one.best_position)
+
+
+def _p2p_rank(rank, world, port, q):
+    import os
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    import torch
+    import torch.distributed as dist
+
+    import paper_2110_01470_b200 as P
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    fn = P.make_function("f4", 64)
+    p = P.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=fn.var_min, var_max=fn.var_max,
+                    nsol=5000, nvar=64, niter=25)
+    rec = P.run_parallel_distributed(p, fn, 11, exchange="p2p")
+    q.put((rank, rec.trajectory.tobytes(), rec.best_position.tobytes()))
+    dist.destroy_process_group()
+
+
+def test_p2p_exchange_across_processes_via_cuda_ipc():
+    """Two processes (gloo only for the one-time IPC-handle exchange) on one GPU."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_p2p_rank, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    out = [q.get(timeout=300) for _ in procs]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    fn = _fn("f4", 64)
+    one = psso.run_parallel(_params(fn, 5000, 25), fn, 11)
+    for _, traj, best in out:
+        assert traj == one.trajectory.tobytes() and best == one.best_position.tobytes()

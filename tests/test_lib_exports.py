@@ -15,7 +15,7 @@ LIB = ROOT / "paper_2110_01470_b200" / "libpsso.so"
 
 def _declared():
     text = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
-    return sorted(set(re.findall(r"\b(psso_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(psso_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_header_declares_the_binding_list():
