@@ -38,3 +38,10 @@ recs = psso.run_parallel_batch(psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=-5
                                               nsol=4096, nvar=128, niter=3),
                                psso.make_function("f5", 128), [1, 2, 3])
 print("ok batch (global-memory exchange)", len(recs), flush=True)
+from paper_2110_01470_b200.sharded import run_virtual_shards  # noqa: E402
+
+fn = psso.make_function("f4", 64)
+rec = run_virtual_shards(psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=fn.var_min,
+                                        var_max=fn.var_max, nsol=3000, nvar=64, niter=4),
+                         fn, 2, 3, exchange="p2p")
+print("ok virtual shards, P2P exchange", flush=True)
