@@ -206,7 +206,8 @@ def run_ours(args, wl):
     import paper_2110_01470_b200 as psso
     from paper_2110_01470_b200 import _lib
     from paper_2110_01470_b200.engine import DeviceEngine, make_config
-    from paper_2110_01470_b200.sharded import ProcessGroupExchange, ShardedDriver, partition
+    from paper_2110_01470_b200.sharded import (P2PExchange, ProcessGroupExchange, ShardedDriver,
+                                               partition)
 
     fn = psso.make_function(fid, nvar)
     nsol = nsol_rank * ws
@@ -217,7 +218,9 @@ def run_ours(args, wl):
     L = _lib.load()
     es = 8 if dtype == "float64" else 4
     if ws > 1:
-        drv = ShardedDriver([eng], ProcessGroupExchange(), ws)
+        ex = (P2PExchange([eng], distributed=True) if args.exchange == "p2p"
+              else ProcessGroupExchange())
+        drv = ShardedDriver([eng], ex, ws)
         with torch.cuda.stream(eng.stream):
             drv.initialize()
             drv.run(0, args.warmup)
@@ -262,6 +265,9 @@ def run_ours(args, wl):
         ms, kern_ms = float(t[0]), float(t[1])
     else:
         kern_ms = kms.value / max(kn.value, 1)  # per iteration
+    if ws > 1 and args.exchange == "p2p":
+        dist.barrier()  # every rank finished reading peer buffers before unmapping
+        ex.close()
     eng.close()
     del eng
     torch.cuda.empty_cache()
@@ -313,8 +319,10 @@ def run_ours(args, wl):
                    "hbm_gbs_per_gpu": 3 * es * nsol * nvar * args.steps / (ms * 1e-3) / 1e9 / ws,
                    "l2": f"inputs larger than L2: X+P = {2 * es * rows_rank * nvar / 2**30:.2f} GiB "
                          f"per GPU vs 126 MB L2",
-                   "parallelism": f"particle shards x{ws}" + (" + NCCL all-gather of gBest "
-                                                             "candidates per iteration" if ws > 1 else "")},
+                   "parallelism": f"particle shards x{ws}" + (
+                       (" + NCCL all-gather of gBest candidates per iteration" if args.exchange == "collective"
+                        else " + device-initiated P2P stores of gBest candidates per iteration")
+                       if ws > 1 else "")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": _traffic(wl, kname), "peak_source": peak_src,
                      "kernel": kname, "kernel_ms_per_iteration": kern_ms,
@@ -340,6 +348,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--rng", default="reference", choices=["reference", "philox"])
+    ap.add_argument("--exchange", default="collective", choices=["collective", "p2p"],
+                    help="N > 1: gBest records by NCCL all-gather or device-initiated P2P stores")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg (diagnostics)")
     args = ap.parse_args()
     if args.warmup < 3:
