@@ -696,3 +696,42 @@ def test_p2p_exchange_across_processes_via_cuda_ipc():
     one = psso.run_parallel(_params(fn, 5000, 25), fn, 11)
     for _, traj, best in out:
         assert traj == one.trajectory.tobytes() and best == one.best_position.tobytes()
+
+
+def test_more_than_2_31_coordinates():
+    """2^25 + 3 particles x 64 = 2.1e9 coordinates per matrix (32 GiB of X + P): 64-bit indexing.
+
+    The last particle (coordinates beyond 2^31) is checked exactly against the
+    keyed RNG: its initial row (core.py:198-199) and its first search step
+    (core.py:129-135), recomputed on the host from RngStream draws.
+    """
+    fn = _fn("f4", 64)
+    n = (1 << 25) + 3
+    p = _params(fn, n, 2)
+    eng = DeviceEngine(p, fn, 21)
+    rng = psso.RngStream(21)
+    j = np.arange(64, dtype=np.uint64)
+    span = p.var_max - p.var_min
+    try:
+        eng.initialize()
+        eng.check()
+        x0 = eng.sol[-1].cpu().numpy()
+        u0 = rng.uniform(psso.SubStream.INIT, 0, n - 1, j)
+        assert np.array_equal(x0, p.var_min + span * u0)
+        g = eng.gbest.cpu().numpy()
+        eng.run(0, 1)
+        eng.check()
+        x1 = eng.sol[-1].cpu().numpy()
+        ub = rng.uniform(psso.SubStream.BRANCH, 0, n - 1, j)
+        uf = rng.uniform(psso.SubStream.FRESH, 0, n - 1, j)
+        want = np.where(ub < p.cw, x0, np.where(ub < p.cp, x0, np.where(ub < p.cg, g,
+                                                                          p.var_min + span * uf)))
+        assert np.array_equal(x1, want)  # pbest == initial row after initialization
+        torch.cuda.synchronize()
+        X, P, p_f = eng.sol, eng.pbests, eng.p_f
+        assert float(X.min()) >= p.var_min and float(X.max()) <= p.var_max
+        b = int(torch.argmin(p_f))
+        assert float(eng.g_f[0]) == float(p_f[b]) == float(p_f.min())
+        assert torch.equal(eng.gbest, P[b])
+    finally:
+        eng.close()
