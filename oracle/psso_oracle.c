@@ -364,3 +364,44 @@ int oracle_max_threads(void) {
 
 /* unused helper kept static-clean */
 int oracle_argmin(const double* f, int64_t n) { return argmin_lex(f, n); }
+
+/* ------------------------------------------------ sequential schedule ---- */
+/* run_sequential loop body (core.py:224-243): the same keyed draws as the
+ * parallel schedule (_draw_update_fields over all rows, core.py:225), but
+ * particles are updated one at a time in index order against the LIVE gbest,
+ * and gbest moves as soon as a particle's new pbest is <= g_f (core.py:236-241).
+ * Non-finite fitness: the row is already in X (core.py:231), nothing else is
+ * written, and the first such particle is reported (core.py:233-234).
+ * Returns 0, or 1 with *bad_i set (sol_f[*bad_i] holds the value). */
+int oracle_step_seq(const oracle_cfg* c, int64_t t, double* X, double* P, double* sol_f,
+                    double* p_f, double* gbest, double* g_f, int64_t* bad_i) {
+    const int64_t N = c->nsol, D = c->nvar;
+    double* s = (double*)malloc(sizeof(double) * (size_t)(D + 4));
+    for (int64_t i = 0; i < N; ++i) {
+        search_rows(c, t, X, P, gbest, i, i + 1);
+        const double fx = fitness_row(c->fid, D, X + i * D, s);
+        sol_f[i] = fx;
+        if (!isfinite(fx)) { *bad_i = i; free(s); return 1; }
+        if (fx <= p_f[i]) {
+            memcpy(P + i * D, X + i * D, sizeof(double) * (size_t)D);
+            p_f[i] = fx;
+            if (fx <= *g_f) {
+                memcpy(gbest, P + i * D, sizeof(double) * (size_t)D);
+                *g_f = fx;
+            }
+        }
+    }
+    free(s);
+    return 0;
+}
+
+/* run_sequential's loop (core.py:222-244); traj[t - t0] = g_f after iteration t. */
+int oracle_run_seq(const oracle_cfg* c, int64_t t0, int64_t niter, double* X, double* P,
+                   double* sol_f, double* p_f, double* gbest, double* g_f, double* traj,
+                   int64_t* bad_t, int64_t* bad_i) {
+    for (int64_t t = t0; t < t0 + niter; ++t) {
+        if (oracle_step_seq(c, t, X, P, sol_f, p_f, gbest, g_f, bad_i)) { *bad_t = t; return 1; }
+        traj[t - t0] = *g_f;
+    }
+    return 0;
+}

@@ -39,3 +39,11 @@ def golden_fitness():
 @pytest.fixture(scope="session")
 def golden_rng():
     return np.load(GOLDEN / "rng.npz")
+
+
+@pytest.fixture(scope="session")
+def golden_seq_runs():
+    """Reference run_sequential results (tests/golden/make_seq_golden.py)."""
+    index = json.loads((GOLDEN / "seq_runs.json").read_text())
+    arrays = np.load(GOLDEN / "seq_runs.npz")
+    return index, arrays
