@@ -112,6 +112,22 @@ int psso_step(psso_ctx* ctx, int64_t t);
  * fused + gBest kernel pair from a captured CUDA graph. */
 int psso_run(psso_ctx* ctx, int64_t t0, int64_t niter);
 
+/* replaces: the loop of run_sequential (core.py:222-244), the per-particle
+ * asynchronous schedule: particles updated in index order against the LIVE
+ * gbest, which moves as soon as a new pbest is <= g_f (core.py:236-241).
+ * Same keyed draws as psso_run; trajectory[t] = g_f after iteration t.  ONE
+ * launch (k_seq): each iteration runs as speculative passes -- all remaining
+ * particles computed in parallel against the current gbest, the prefix up to
+ * the first gbest move (or non-finite fitness) committed, the next pass
+ * starting after it -- so results are bit-identical to the serial loop.
+ * Unsharded contexts, nvar <= 128 (else PSSO_E_INVALID / PSSO_E_UNSUPPORTED).
+ * Call psso_init first (core.py:220).  Asynchronous. */
+int psso_run_sequential(psso_ctx* ctx, int64_t t0, int64_t niter);
+
+/* Passes k_seq ran in the last psso_run_sequential (iterations + gbest moves
+ * when nothing is non-finite).  Synchronizes the stream. */
+int psso_sequential_passes(psso_ctx* ctx, int64_t* passes);
+
 /* Name of the iteration kernel psso_run uses for this configuration
  * (k_swarm / k_chain / k_rows / k_fused / k_tile with its template arguments). */
 const char* psso_kernel_name(const psso_ctx* ctx);

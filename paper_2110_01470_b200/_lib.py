@@ -34,7 +34,7 @@ EXPORTS = (
     "psso_rng_uniform", "psso_eval_rows", "psso_solve", "psso_profile", "psso_profile_read",
     "psso_kernel_name", "psso_solve_batch", "psso_p2p_buffer_bytes", "psso_p2p_alloc",
     "psso_p2p_free", "psso_p2p_handle", "psso_p2p_open", "psso_p2p_close", "psso_publish_p2p",
-    "psso_apply_p2p",
+    "psso_apply_p2p", "psso_run_sequential", "psso_sequential_passes",
 )
 
 
@@ -131,6 +131,8 @@ def load():
     L.psso_p2p_close.argtypes = [vp]
     L.psso_publish_p2p.argtypes = [vp, vp, vp, i32, i32, u64]
     L.psso_apply_p2p.argtypes = [vp, i64, vp, i32, u64, i32]
+    L.psso_run_sequential.argtypes = [vp, i64, i64]
+    L.psso_sequential_passes.argtypes = [vp, ctypes.POINTER(i64)]
     for name in EXPORTS:
         if not hasattr(L, name):
             raise RuntimeError(f"{LIB_PATH} does not export {name}")

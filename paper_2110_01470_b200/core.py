@@ -19,6 +19,7 @@ __all__ = [
     "NonFiniteFitnessError",
     "step_update_variable",
     "initialize",
+    "run_sequential",
 ]
 
 
@@ -125,3 +126,53 @@ def initialize(params: SsoParams, f, rng, *, dtype: str = "float64") -> Swarm:
         return eng.to_host()
     finally:
         eng.close()
+
+
+def run_sequential(params: SsoParams, f, seed: int, *, dtype: str = "float64",
+                   rng: str = "reference", device=None):
+    """The per-particle asynchronous schedule (core.py:213-258) on the GPU.
+
+    Particles are updated in index order against the live gBest, which moves
+    as soon as a particle's new pBest is ``<=`` g_f (core.py:236-241); same
+    keyed draws as ``run_parallel``.  The whole loop is ONE kernel launch
+    (``psso_run_sequential``): each iteration runs as speculative passes over
+    the remaining particles, committing the prefix up to the first gBest move,
+    so the result is bit-identical to the serial loop.  ``wall_time_s`` is the
+    loop-only device time (core.py:222,245).  Needs ``nvar <= 128``.
+    """
+    import torch
+
+    from .engine import DeviceEngine
+    from .records import RunRecord, ScheduleKind
+
+    eng = DeviceEngine(params, f, seed, dtype=dtype, rng=rng, device=device)
+    try:
+        eng.initialize()
+        start = torch.cuda.Event(enable_timing=True)
+        stop = torch.cuda.Event(enable_timing=True)
+        start.record(eng.stream)
+        eng.run_sequential(0, params.niter)
+        stop.record(eng.stream)
+        eng.check()
+        wall = start.elapsed_time(stop) * 1e-3
+        trajectory = eng.traj.cpu().numpy()
+        best_position = eng.gbest.to(torch.float64).cpu().numpy()
+        best = float(eng.g_f.cpu()[0])
+    finally:
+        eng.close()
+    return RunRecord(
+        run_id=0,
+        schedule=ScheduleKind.SEQUENTIAL,
+        function=getattr(f, "id", "custom"),
+        nsol=params.nsol,
+        nvar=params.nvar,
+        niter=params.niter,
+        cw=params.cw,
+        cp=params.cp,
+        cg=params.cg,
+        seed=seed,
+        best_fitness=best,
+        wall_time_s=wall,
+        best_position=best_position,
+        trajectory=trajectory,
+    )

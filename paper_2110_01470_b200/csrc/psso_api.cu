@@ -15,6 +15,7 @@
 #include "psso.h"
 #include "psso_device.cuh"
 #include "psso_registry.h"
+#include "psso_seq.cuh"
 #include "psso_swarm.cuh"
 
 using namespace psso;
@@ -457,6 +458,12 @@ struct psso_ctx {
   int32_t* sw_slot_new;
   void* sw_slot_row;
   uint64_t* sw_seed;
+  // sequential schedule (psso_seq.cuh), allocated on first use
+  void* seq_xn;          // rows x D speculative rows
+  double* seq_fn;        // rows speculative fitness
+  double* seq_pfn;       // rows scratch
+  uint64_t* seq_seed;
+  int64_t* seq_passes;
   std::string kname;     // the iteration kernel psso_run launches (psso_kernel_name)
   std::string err;
 };
@@ -986,6 +993,11 @@ void psso_destroy(psso_ctx* c) {
   cudaFree(c->sw_slot_i);
   cudaFree(c->sw_slot_row);
   cudaFree(c->sw_seed);
+  cudaFree(c->seq_xn);
+  cudaFree(c->seq_fn);
+  cudaFree(c->seq_pfn);
+  cudaFree(c->seq_seed);
+  cudaFree(c->seq_passes);
   delete c;
 }
 
@@ -1133,6 +1145,71 @@ int psso_run(psso_ctx* c, int64_t t0, int64_t niter) {
     int rc = fused_step(c, t0 + done, nullptr);
     if (rc) return rc;
   }
+  return PSSO_OK;
+}
+
+// run_sequential (core.py:213-258): one k_seq launch for the whole loop
+// (speculative passes with rollback, psso_seq.cuh).
+int psso_run_sequential(psso_ctx* c, int64_t t0, int64_t niter) {
+  if (int rc = need_bound(c)) return rc;
+  if (t0 < 0 || niter < 0) return fail(c, PSSO_E_INVALID, "t0 and niter must be >= 0");
+  const psso_config* cfg = &c->cfg;
+  if (cfg->row_lo != 0 || cfg->row_hi != cfg->nsol)
+    return fail(c, PSSO_E_INVALID, "the sequential schedule runs unsharded swarms only");
+  if (!c->chain)
+    return fail(c, PSSO_E_UNSUPPORTED, "the sequential schedule supports nvar <= 128 (chain-mapped rows)");
+  const int64_t rows = cfg->nsol, D = cfg->nvar;
+  const int M = D <= 32 ? 4 : D <= 64 ? 8 : 16;
+  const int es = cfg->dtype == PSSO_F64 ? 8 : 4;
+  const int nw = PSSO_SEQ_NT / 32;
+  const bool smem_fn = cfg->fn_id == 3 || cfg->fn_id == 7 || cfg->fn_id == 8;
+  const void* f = seq_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, M);
+  if (!f) return fail(c, PSSO_E_UNSUPPORTED, "no sequential kernel for this configuration");
+  if (!c->seq_xn) {
+    const uint64_t seed = cfg->seed;
+    CK(c, cudaMalloc(&c->seq_xn, (size_t)rows * D * es));
+    CK(c, cudaMalloc(&c->seq_fn, (size_t)rows * sizeof(double)));
+    CK(c, cudaMalloc(&c->seq_pfn, (size_t)rows * sizeof(double)));
+    CK(c, cudaMalloc(&c->seq_seed, sizeof(uint64_t)));
+    CK(c, cudaMalloc(&c->seq_passes, sizeof(int64_t)));
+    CK(c, cudaMemcpy(c->seq_seed, &seed, sizeof seed, cudaMemcpyHostToDevice));
+    CK(c, cudaMemset(c->seq_passes, 0, sizeof(int64_t)));
+  }
+  if (niter == 0) return PSSO_OK;
+  TileParams p = tile_params(c, M_SOLF, t0, nullptr, false);
+  p.off_red = (int)align16((size_t)8 * M * es);
+  p.off_bar = (int)align16((size_t)p.off_red + 16 * nw + 64 * M);
+  p.off_scr = (int)align16((size_t)p.off_bar + 8 * (nw + 1));
+  const size_t smem = (size_t)p.off_scr + (smem_fn ? (size_t)nw * 4 * (8 * M) * es : 0);
+  CK(c, cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SeqParams q;
+  std::memset(&q, 0, sizeof q);
+  q.t0 = t0;
+  q.niter = niter;
+  q.rows = rows;
+  q.Xn = c->seq_xn;
+  q.fn = c->seq_fn;
+  q.pfn = c->seq_pfn;
+  q.traj = c->buf.traj;
+  q.traj_stride = 0;
+  q.g_f = c->buf.g_f;
+  q.gbest = c->buf.gbest;
+  q.seeds = c->seq_seed;
+  q.sol_f = c->buf.sol_f;
+  q.bad = c->bad;
+  q.passes = c->seq_passes;
+  void* args[] = {(void*)&p, (void*)&q};
+  CK(c, cudaLaunchKernel(f, dim3(1, 1), dim3(PSSO_SEQ_NT), args, smem, c->stream));
+  c->launches++;
+  return PSSO_OK;
+}
+
+int psso_sequential_passes(psso_ctx* c, int64_t* passes) {
+  if (!c || !passes) return fail(c, PSSO_E_INVALID, "null argument");
+  *passes = 0;
+  if (!c->seq_passes) return PSSO_OK;
+  CK(c, cudaStreamSynchronize(c->stream));
+  CK(c, cudaMemcpy(passes, c->seq_passes, sizeof(int64_t), cudaMemcpyDeviceToHost));
   return PSSO_OK;
 }
 

@@ -1,0 +1,200 @@
+// psso_seq.cuh -- the reference's SEQUENTIAL (per-particle asynchronous)
+// schedule, run_sequential (core.py:213-258), on device.
+//
+// The schedule is serial by definition: particle i is updated against the
+// gbest left by particles 0..i-1 of the same iteration, and gbest moves the
+// moment a particle's new pbest is <= g_f (core.py:236-241).  The draws do not
+// depend on the state (keyed RNG, core.py:225), so the only serial coupling is
+// gbest, and gbest moves rarely (a few dozen times per run, SURVEY appendix A
+// / tests/golden/seq_runs.json).  k_seq therefore runs the iteration as
+// SPECULATIVE PASSES with rollback:
+//
+//   pass from row lo: every row r >= lo is computed in parallel against the
+//   current gbest (chain_step: draw + select + fitness in numpy order) into a
+//   scratch row Xn[r] and fn[r] -- nothing of the swarm is written;
+//   the first event r* >= lo = first row whose fitness is non-finite or is a
+//   gbest move (fn <= p_f and fn <= g_f) -- a block-wide min;
+//   rows lo..r* are exactly what the serial loop would produce (none of them
+//   saw a gbest change), so they are committed (X, sol_f, pBest <=); the
+//   gbest move of r* is applied; the next pass starts at r* + 1.
+//
+// An iteration costs 1 + (gbest moves in it) passes; the results are
+// bit-identical to the serial loop.  One CTA per swarm (blockIdx.y = swarm of
+// a batch), the swarm's rows in global memory (L2-resident at the sizes this
+// schedule is used at), gbest in shared memory.
+#pragma once
+
+#include "psso_device.cuh"
+
+namespace psso {
+
+#ifndef PSSO_SEQ_NT
+#define PSSO_SEQ_NT 512
+#endif
+
+struct SeqParams {
+  int64_t t0, niter;
+  int64_t rows;             // rows per swarm
+  void* Xn;                 // [B][rows][D] speculative rows (scratch)
+  double* fn;               // [B][rows] speculative fitness (scratch)
+  double* pfn;              // [B][rows] scratch for chain_step's p_f writes (unused values)
+  double* traj;             // [B][traj_stride] (indexed by t) or null
+  int64_t traj_stride;
+  double* g_f;              // [B]
+  void* gbest;              // [B][D]
+  const uint64_t* seeds;    // [B]
+  double* sol_f;            // [B][rows] or null
+  unsigned long long* bad;  // [B]: min((t+1) << 40 | i) of the first non-finite fitness
+  int64_t* passes;          // [B] passes run (diagnostic) or null
+};
+
+// Shared memory (offsets in TileParams):
+//   0        gbest (8M entries of T; entries past D are read and discarded)
+//   off_red  warp reduction (16 * NW) + xs30(gamma*(j+1)) table (8 * 8M)
+//   off_bar  first-event reduction: NW int64 + 1
+//   off_scr  per-warp smem rows [4][8M] (f3, f7, f8)
+template <typename T, int FN, int RNG, int M>
+__global__ void __launch_bounds__(PSSO_SEQ_NT, 1)
+    k_seq(const __grid_constant__ TileParams p, const __grid_constant__ SeqParams q) {
+  constexpr int NTC = PSSO_SEQ_NT;
+  constexpr int NW = NTC / 32;
+  extern __shared__ __align__(128) unsigned char smem[];
+  T* gb = reinterpret_cast<T*>(smem);
+  uint64_t* xg = reinterpret_cast<uint64_t*>(smem + p.off_red + 16 * NW);  // [8M]
+  int64_t* red = reinterpret_cast<int64_t*>(smem + p.off_bar);            // [NW + 1]
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int k = lane & 7;
+  const int b = blockIdx.y;
+  const int D = p.D;
+  const int64_t rows = q.rows;
+  const int64_t ngroups = (rows + 3) >> 2;
+  T* scr = reinterpret_cast<T*>(smem + p.off_scr) + warp * 4 * (8 * M);
+
+  T* X = reinterpret_cast<T*>(p.X) + (int64_t)b * rows * D;
+  T* P = reinterpret_cast<T*>(p.P) + (int64_t)b * rows * D;
+  double* pf = p.p_f + (int64_t)b * rows;
+  T* Xn = reinterpret_cast<T*>(q.Xn) + (int64_t)b * rows * D;
+  double* fn = q.fn + (int64_t)b * rows;
+  double* sf = q.sol_f ? q.sol_f + (int64_t)b * rows : nullptr;
+  T* gbp = reinterpret_cast<T*>(q.gbest) + (int64_t)b * D;
+  unsigned long long* bad = q.bad + b;
+  if (*(volatile unsigned long long*)bad != ~0ull) return;  // an earlier non-finite fitness
+
+  // chain_step writes its row to ev.X (and, when it improves, again to ev.P),
+  // its fitness to ev.sol_f and improved fitness to ev.p_f: all scratch here
+  ChainEnv ev;
+  ev.X = Xn;
+  ev.P = Xn;
+  ev.p_f = q.pfn + (int64_t)b * rows;
+  ev.sol_f = fn;
+  ev.bad = nullptr;
+  ev.row_lo = 0;
+  ev.seed = q.seeds[b];
+  ev.D = D;
+  ev.n = p.plan.n;
+  ev.mlen = ev.n >= 8 ? (ev.n >> 3) : 0;
+  ev.tail = ev.n - 8 * ev.mlen;
+  ev.rootb = ev.rootf = 0;
+
+  for (int q8 = tid; q8 < 8 * M; q8 += NTC) {
+    xg[q8] = xs30(GAMMA * (uint64_t)(q8 + 1));
+    gb[q8] = q8 < D ? gbp[q8] : (T)0;
+  }
+  double gf = q.g_f[b];
+  int64_t npass = 0;
+  bool stop = false;
+  __syncthreads();
+
+  for (int64_t it = 0; it < q.niter && !stop; ++it) {
+    const int64_t t = q.t0 + it;
+    ev.t = t;
+    if constexpr (RNG == 0) {
+      ev.rootb = root64(ev.seed, STREAM_BRANCH, (uint64_t)t);
+      ev.rootf = root64(ev.seed, STREAM_FRESH, (uint64_t)t);
+    }
+    int64_t lo = 0;
+    while (lo < rows) {
+      ++npass;
+      // ---- speculative pass over rows [lo, rows) (core.py:227-232 for every row at once)
+      double best_f = CUDART_INF;
+      int64_t best_i = INT64_MAX;
+      int best_new = 0;
+      for (int64_t grp = (lo >> 2) + warp; grp < ngroups; grp += NW) {
+        const int64_t r = 4 * grp + (lane >> 3);
+        const bool rv = r < rows && r >= lo;
+        const int64_t rl = r < rows ? r : rows - 1;
+        const double pf_row = pf[rl];
+        const T* xl = X + rl * (int64_t)D;
+        const T* pl = P + rl * (int64_t)D;
+        T x[M], pv[M];
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          const int j = k + 8 * m;
+          x[m] = j < D ? xl[j] : (T)0;
+          pv[m] = j < D ? pl[j] : (T)0;
+        }
+        chain_step<T, FN, RNG, M, false, false, true>(p, ev, gb, xg, scr, r, rv, x, pv, pf_row,
+                                                      best_f, best_i, best_new);
+      }
+      __syncthreads();  // Xn / fn of the pass visible to the block
+      // ---- first event r* >= lo: non-finite (core.py:233) or a gbest move (core.py:236-241)
+      int64_t ev_r = INT64_MAX;
+      for (int64_t r = lo + tid; r < rows; r += NTC) {
+        const double f = fn[r];
+        if (!isfinite(f) || (f <= pf[r] && f <= gf)) { ev_r = r; break; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ev_r = min(ev_r, __shfl_xor_sync(0xffffffffu, ev_r, o));
+      if (lane == 0) red[warp] = ev_r;
+      __syncthreads();
+      if (warp == 0) {
+        int64_t v = lane < NW ? red[lane] : INT64_MAX;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (lane == 0) red[NW] = v;
+      }
+      __syncthreads();
+      const int64_t rs = red[NW];
+      const int64_t hi = rs < rows ? rs : rows - 1;  // last committed row
+      // ---- commit rows lo..hi: X always (core.py:231), pBest on `<=` (core.py:236-238)
+      for (int64_t r = lo + warp; r <= hi; r += NW) {
+        const double f = fn[r];
+        const bool imp = isfinite(f) && f <= pf[r];
+        const T* src = Xn + r * (int64_t)D;
+        for (int j = lane; j < D; j += 32) {
+          const T v = src[j];
+          X[r * (int64_t)D + j] = v;
+          if (imp) P[r * (int64_t)D + j] = v;
+        }
+      }
+      __syncthreads();  // pBest rows copied before p_f moves
+      for (int64_t r = lo + tid; r <= hi; r += NTC) {
+        const double f = fn[r];
+        if (sf) sf[r] = f;
+        if (isfinite(f) && f <= pf[r]) pf[r] = f;
+      }
+      if (rs < rows) {
+        const double f = fn[rs];
+        if (!isfinite(f)) {
+          if (tid == 0) *bad = ((unsigned long long)(t + 1) << 40) | (unsigned long long)rs;
+          stop = true;
+        } else {  // gbest <- pbests[r*] (core.py:239-241)
+          for (int j = tid; j < D; j += NTC) gb[j] = Xn[rs * (int64_t)D + j];
+          gf = f;
+        }
+      }
+      __syncthreads();
+      if (stop) break;
+      lo = rs < rows ? rs + 1 : rows;
+    }
+    if (!stop && tid == 0 && q.traj) q.traj[b * q.traj_stride + t] = gf;  // core.py:242
+  }
+  for (int j = tid; j < D; j += NTC) gbp[j] = gb[j];
+  if (tid == 0) {
+    q.g_f[b] = gf;
+    if (q.passes) q.passes[b] = npass;
+  }
+}
+
+}  // namespace psso

@@ -1,6 +1,7 @@
 // psso_swarm_inst.cuh -- k_swarm instantiations for one (T, RNG) pair.
 // Included by psso_swarm_{f64,f32}_{ref,philox}.cu with PSSO_T, PSSO_RNG and
 // PSSO_NAME(x) defined.
+#include "psso_seq.cuh"
 #include "psso_swarm.cuh"
 #include "psso_registry.h"
 
@@ -20,6 +21,22 @@ const void* PSSO_NAME(swarm_kernel)(int fn, int m, bool res, bool cl) {
   switch (fn) {
     PSSO_SWARM(0) PSSO_SWARM(1) PSSO_SWARM(2) PSSO_SWARM(3) PSSO_SWARM(4)
     PSSO_SWARM(5) PSSO_SWARM(6) PSSO_SWARM(7) PSSO_SWARM(8) PSSO_SWARM(9)
+    default:
+      return nullptr;
+  }
+}
+
+#define PSSO_SEQ(FN)                                                    \
+  case FN:                                                              \
+    if (m == 4) return (const void*)k_seq<PSSO_T, FN, PSSO_RNG, 4>;     \
+    if (m == 8) return (const void*)k_seq<PSSO_T, FN, PSSO_RNG, 8>;     \
+    if (m == 16) return (const void*)k_seq<PSSO_T, FN, PSSO_RNG, 16>;   \
+    return nullptr;
+
+const void* PSSO_NAME(seq_kernel)(int fn, int m) {
+  switch (fn) {
+    PSSO_SEQ(0) PSSO_SEQ(1) PSSO_SEQ(2) PSSO_SEQ(3) PSSO_SEQ(4)
+    PSSO_SEQ(5) PSSO_SEQ(6) PSSO_SEQ(7) PSSO_SEQ(8) PSSO_SEQ(9)
     default:
       return nullptr;
   }

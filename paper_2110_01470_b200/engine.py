@@ -116,6 +116,17 @@ class DeviceEngine:
         """The run_parallel loop (parallel.py:192-212), asynchronous on self.stream."""
         self._call("psso_run", int(t0), int(niter))
 
+    def run_sequential(self, t0: int, niter: int):
+        """The run_sequential loop (core.py:222-244), asynchronous on self.stream."""
+        self._call("psso_run_sequential", int(t0), int(niter))
+
+    @property
+    def sequential_passes(self) -> int:
+        """Speculative passes of the last run_sequential (iterations + gBest moves)."""
+        n = ctypes.c_int64(0)
+        self._call("psso_sequential_passes", ctypes.byref(n))
+        return int(n.value)
+
     def search(self, t):
         self._call("psso_search", int(t))
 

@@ -1,0 +1,179 @@
+"""GPU parity of the sequential schedule (reference core.py:213-258) on device.
+
+``run_sequential`` runs ONE k_seq launch (speculative passes with rollback,
+psso_seq.cuh).  Checked against fixtures made by the reference's own
+run_sequential (tests/golden/make_seq_golden.py) and against the oracle's C
+restatement: positions, pBests and gBest bitwise, fitness bitwise for f1-f4 and
+within RTOL for the transcendental objectives.
+"""
+
+import json
+import math
+import warnings
+
+import numpy as np
+import pytest
+
+from conftest import BITWISE_FIDS, GOLDEN
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU runs deselect -m gpu
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2110_01470_b200 as psso  # noqa: E402
+from oracle import oracle as O  # noqa: E402  (the checker)
+from paper_2110_01470_b200.engine import DeviceEngine  # noqa: E402
+
+RTOL = 1e-12
+
+SEQ_INDEX = {e["key"]: e for e in json.loads((GOLDEN / "seq_runs.json").read_text())}
+
+
+def _fn(fid, d):
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        return psso.make_function(fid, d)
+
+
+def _close(a, b, fid):
+    a, b = np.asarray(a), np.asarray(b)
+    if fid in BITWISE_FIDS:
+        return np.array_equal(a, b)
+    return np.allclose(a, b, rtol=RTOL, atol=0.0)
+
+
+def _params_of(e):
+    return psso.SsoParams(cw=e["cw"], cp=e["cp"], cg=e["cg"], var_min=e["var_min"],
+                          var_max=e["var_max"], nsol=e["nsol"], nvar=e["nvar"], niter=e["niter"])
+
+
+@pytest.mark.parametrize("key", sorted(SEQ_INDEX, key=lambda k: int(k[3:])))
+def test_run_sequential_against_reference_golden(key, golden_seq_runs):
+    e = SEQ_INDEX[key]
+    _, arr = golden_seq_runs
+    fn = _fn(e["fid"], e["nvar"])
+    p = _params_of(e)
+    rec = psso.run_sequential(p, fn, seed=e["seed"])
+    assert rec.schedule == psso.ScheduleKind.SEQUENTIAL and rec.function == e["fid"]
+    assert np.array_equal(rec.best_position, arr[key + "_gbest"]), "gbest position (bitwise)"
+    assert _close(rec.trajectory, arr[key + "_traj"], e["fid"]), "trajectory"
+    assert rec.best_fitness == rec.trajectory[-1]
+    # end state, and the pass count of the rollback scheme: one pass per
+    # iteration plus one per gbest move
+    eng = DeviceEngine(p, fn, e["seed"])
+    try:
+        eng.initialize()
+        eng.run_sequential(0, p.niter)
+        eng.check()
+        sw = eng.to_host()
+        passes = eng.sequential_passes
+    finally:
+        eng.close()
+    assert np.array_equal(sw.sol, arr[key + "_sol"])
+    assert np.array_equal(sw.pbests, arr[key + "_pbests"])
+    assert _close(sw.p_f, arr[key + "_p_f"], e["fid"])
+    assert _close(sw.sol_f, arr[key + "_sol_f"], e["fid"])
+    assert passes <= p.niter + e["gbest_moves"]
+    assert passes >= p.niter
+
+
+def test_c1_sequential_appendix_value():
+    fn = psso.make_function("f1", 30)
+    p = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=-5.12, var_max=5.12, nsol=100, nvar=30,
+                       niter=1000)
+    rec = psso.run_sequential(p, fn, seed=0)
+    assert rec.best_fitness == 10.383304882651581  # SURVEY appendix A (reference run_sequential)
+
+
+@pytest.mark.parametrize("fid,nsol,nvar,niter", [
+    ("f1", 1000, 32, 30), ("f2", 517, 50, 20), ("f3", 300, 64, 15), ("f4", 2000, 64, 10),
+    ("f5", 700, 128, 12), ("f6", 333, 100, 12), ("f7", 400, 77, 12), ("f8", 250, 40, 12),
+    ("f9", 600, 13, 15),
+])
+def test_sequential_against_oracle(fid, nsol, nvar, niter):
+    fn = _fn(fid, nvar)
+    p = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=fn.var_min, var_max=fn.var_max,
+                       nsol=nsol, nvar=nvar, niter=niter)
+    o = O.Oracle.from_params(p, fid, 23)
+    osw = o.initialize()
+    otraj = o.run_sequential(osw, 0, niter)
+    eng = DeviceEngine(p, fn, 23)
+    try:
+        eng.initialize()
+        eng.run_sequential(0, niter)
+        eng.check()
+        sw = eng.to_host()
+        traj = eng.traj.cpu().numpy()
+    finally:
+        eng.close()
+    assert np.array_equal(sw.sol, osw.sol)
+    assert np.array_equal(sw.pbests, osw.pbests)
+    assert np.array_equal(sw.gbest, osw.gbest)
+    assert _close(traj, otraj, fid)
+    assert _close(sw.p_f, osw.p_f, fid)
+
+
+def test_sequential_continues_across_calls():
+    """Two psso_run_sequential calls == one call over the whole range."""
+    fn = psso.make_function("f4", 20)
+    p = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=fn.var_min, var_max=fn.var_max,
+                       nsol=150, nvar=20, niter=40)
+    outs = []
+    for split in (None, 17):
+        eng = DeviceEngine(p, fn, 4)
+        try:
+            eng.initialize()
+            if split is None:
+                eng.run_sequential(0, 40)
+            else:
+                eng.run_sequential(0, split)
+                eng.run_sequential(split, 40 - split)
+            outs.append((eng.to_host(), eng.traj.cpu().numpy()))
+        finally:
+            eng.close()
+    assert np.array_equal(outs[0][0].sol, outs[1][0].sol)
+    assert np.array_equal(outs[0][1], outs[1][1])
+
+
+def test_sequential_nonfinite_names_first_particle():
+    """The first (iteration, particle) in serial order whose probe fitness is +inf."""
+    level = float(O.init_positions(0, 40, 4, -1.0, 1.0)[:, 0].max())  # init stays finite
+    fn = psso.probe_function(4, level=level, bounds=(-1.0, 1.0))
+    p = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=-1, var_max=1, nsol=40, nvar=4, niter=200)
+    with pytest.raises(psso.NonFiniteFitnessError) as ei:
+        psso.run_sequential(p, fn, seed=0)
+    err = ei.value
+    assert err.iteration is not None and math.isinf(err.value)
+    # the probe is Sphere until it fires: replay with the oracle's f1 sequential step
+    o = O.Oracle("f1", 40, 4, 0.3, 0.6, 0.8, -1.0, 1.0, 0)
+    sw = o.initialize()
+    for t in range(p.niter):
+        o.step_sequential(sw, t)
+        bad = np.nonzero(sw.sol[:, 0] > level)[0]
+        if bad.size:
+            assert (t, int(bad[0])) == (err.iteration, err.particle)
+            break
+    else:
+        pytest.fail("oracle replay never hit the probe")
+
+
+def test_sequential_rejects_unsupported_shapes():
+    fn = psso.make_function("f1", 200)
+    p = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=-5.12, var_max=5.12, nsol=10, nvar=200,
+                       niter=3)
+    with pytest.raises(psso._lib.PssoError, match="nvar <= 128"):
+        psso.run_sequential(p, fn, seed=0)
+
+
+def test_sequential_fp32_and_philox_modes_run():
+    fn = psso.make_function("f5", 64)
+    p = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=-5.12, var_max=5.12, nsol=256, nvar=64,
+                       niter=50)
+    for dtype, rng in (("float32", "reference"), ("float64", "philox")):
+        rec = psso.run_sequential(p, fn, seed=3, dtype=dtype, rng=rng)
+        assert np.all(np.diff(rec.trajectory) <= 0)
+        assert np.all(np.abs(rec.best_position) <= 5.12)
+        assert rec.best_fitness == pytest.approx(fn(rec.best_position[None, :].astype(np.float64))[0],
+                                                 rel=1e-5)
