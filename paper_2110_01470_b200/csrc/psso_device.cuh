@@ -1039,7 +1039,23 @@ struct ChainEnv {
   uint64_t rootb, rootf;  // keyed roots of the BRANCH/FRESH (or INIT) streams at t
   int64_t t;
   int D, n, mlen, tail;   // row length, terms, full chains, tail terms
+  const double* aux;      // f7: 1/sqrt(j+1), staged in shared memory by the kernel
 };
+
+// f7's 1/sqrt(j+1) table (benchmarks.py:216) in shared memory for the chain
+// kernels (D <= 128): read once per launch instead of once per coordinate
+// per iteration from global memory.  The whole block must call it.
+template <int FN>
+__device__ __forceinline__ const double* stage_aux(const double* aux, int D) {
+  if constexpr (FN == 7) {
+    __shared__ double aux_s[128];
+    for (int j = threadIdx.x; j < D; j += blockDim.x) aux_s[j] = aux[j];
+    __syncthreads();
+    return aux_s;
+  } else {
+    return aux;
+  }
+}
 
 // One group step of the chain mapping: the segment's row r (rv: r exists;
 // x holds the loaded positions, pv the pbests unless INIT).  Positions, X
@@ -1151,24 +1167,46 @@ __device__ __forceinline__ void chain_step(const TileParams& p, const ChainEnv& 
     for (int m = 0; m < M; ++m) {
       const int j = k + 8 * m;
       if (FULL || j < D) {
-        if constexpr (FN == 7) row[j] = Trig<T>::cos_(N::mul(x[m], (T)p.aux[j]));  // factors
+        if constexpr (FN == 7) row[j] = Trig<T>::cos_(N::mul(x[m], (T)ev.aux[j]));  // factors
         else row[j] = x[m];
       }
     }
     __syncwarp();
+    // the sequential chains run in lane 0 of the segment; their operands are
+    // loaded 8 at a time ahead of the dependent adds/multiplies so only the
+    // fp64 latency of the chain itself is exposed, not the smem latency
     if constexpr (FN == 3) {  // c = cumsum(x) left to right, terms c*c in place
       if (k == 0) {
-        T c = row[0];
-        row[0] = N::mul(c, c);
-        for (int j = 1; j < D; ++j) {
-          c = N::add(c, row[j]);
-          row[j] = N::mul(c, c);
+        T c = (T)0;
+#pragma unroll
+        for (int g = 0; g < M; ++g) {
+          if (8 * g >= D) break;
+          T v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = (8 * g + u < D) ? row[8 * g + u] : (T)0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int j = 8 * g + u;
+            if (j < D) {
+              c = j == 0 ? v[0] : N::add(c, v[u]);
+              row[j] = N::mul(c, c);
+            }
+          }
         }
       }
       __syncwarp();
     } else if constexpr (FN == 7) {  // prod(cos(x * inv)) left to right
-      if (k == 0)
-        for (int j = 0; j < D; ++j) prod = N::mul(prod, row[j]);
+      if (k == 0) {
+#pragma unroll
+        for (int g = 0; g < M; ++g) {
+          if (8 * g >= D) break;
+          T v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = (8 * g + u < D) ? row[8 * g + u] : (T)1;  // x*1 == x
+#pragma unroll
+          for (int u = 0; u < 8; ++u) prod = N::mul(prod, v[u]);
+        }
+      }
       prod = __shfl_sync(0xffffffffu, prod, seg);
     }
   }
@@ -1289,6 +1327,7 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, PSSO_CHAIN_MINB)
   if (!INIT && p.bad && *(volatile unsigned long long*)p.bad != ~0ull) return;
 
   ChainEnv ev;
+  ev.aux = stage_aux<FN>(p.aux, p.D);
   ev.X = p.X;
   ev.P = p.P;
   ev.p_f = p.p_f;

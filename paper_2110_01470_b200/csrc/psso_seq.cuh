@@ -84,6 +84,7 @@ __global__ void __launch_bounds__(PSSO_SEQ_NT, 1)
   // chain_step writes its row to ev.X (and, when it improves, again to ev.P),
   // its fitness to ev.sol_f and improved fitness to ev.p_f: all scratch here
   ChainEnv ev;
+  ev.aux = stage_aux<FN>(p.aux, p.D);
   ev.X = Xn;
   ev.P = Xn;
   ev.p_f = q.pfn + (int64_t)b * rows;

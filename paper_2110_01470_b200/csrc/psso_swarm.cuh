@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(PSSO_SWARM_NT, 1)
   double* pfs = reinterpret_cast<double*>(Ps + (size_t)sp.gpc * 4 * D);
 
   ChainEnv ev;
+  ev.aux = stage_aux<FN>(p.aux, p.D);
   ev.X = RES ? (void*)Xs : (void*)Xg;
   ev.P = RES ? (void*)Ps : (void*)Pg;
   ev.p_f = RES ? pfs : pfg;

@@ -45,3 +45,8 @@ rec = run_virtual_shards(psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=fn.var_m
                                         var_max=fn.var_max, nsol=3000, nvar=64, niter=4),
                          fn, 2, 3, exchange="p2p")
 print("ok virtual shards, P2P exchange", flush=True)
+for fid, n, d, it in (("f1", 100, 30, 20), ("f7", 70, 20, 10), ("f5", 300, 128, 5)):  # k_seq
+    fn = psso.make_function(fid, d)
+    rec = psso.run_sequential(psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=fn.var_min,
+                                             var_max=fn.var_max, nsol=n, nvar=d, niter=it), fn, 2)
+    print("ok sequential", fid, n, d, flush=True)
