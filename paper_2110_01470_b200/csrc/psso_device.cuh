@@ -1162,20 +1162,29 @@ __device__ __forceinline__ void chain_step(const TileParams& p, const ChainEnv& 
   // ---- sequential / grouped objectives: the segment's row in smem
   T* row = scr + (lane >> 3) * (8 * M);
   T prod = (T)1;
-  if constexpr (chain_smem_fn<FN>()) {
+  if constexpr (FN == 7) {
+    // prod(cos(x_j / sqrt(j+1))) left to right (benchmarks.py:143-148): at
+    // each m the segment's 8 lanes hold j = 8m..8m+7, so every lane runs the
+    // same chain over shuffled factors -- no divergence, no smem round trip,
+    // and the factors of m+1 overlap the dependent multiplies of m
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      if (!FULL && 8 * m >= D) break;
+      const int j = k + 8 * m;
+      const T c = (FULL || j < D) ? Trig<T>::cos_(N::mul(x[m], (T)ev.aux[j])) : (T)1;  // x*1 == x
+#pragma unroll
+      for (int u = 0; u < 8; ++u) prod = N::mul(prod, __shfl_sync(0xffffffffu, c, seg + u));
+    }
+  } else if constexpr (chain_smem_fn<FN>()) {
 #pragma unroll
     for (int m = 0; m < M; ++m) {
       const int j = k + 8 * m;
-      if (FULL || j < D) {
-        if constexpr (FN == 7) row[j] = Trig<T>::cos_(N::mul(x[m], (T)ev.aux[j]));  // factors
-        else row[j] = x[m];
-      }
+      if (FULL || j < D) row[j] = x[m];
     }
     __syncwarp();
-    // the sequential chains run in lane 0 of the segment; their operands are
-    // loaded 8 at a time ahead of the dependent adds/multiplies so only the
-    // fp64 latency of the chain itself is exposed, not the smem latency
-    if constexpr (FN == 3) {  // c = cumsum(x) left to right, terms c*c in place
+    if constexpr (FN == 3) {  // c = cumsum(x) left to right, terms c*c in place, in
+      // lane 0 of the segment; operands loaded 8 at a time ahead of the
+      // dependent adds so only the fp64 latency of the chain is exposed
       if (k == 0) {
         T c = (T)0;
 #pragma unroll
@@ -1195,19 +1204,6 @@ __device__ __forceinline__ void chain_step(const TileParams& p, const ChainEnv& 
         }
       }
       __syncwarp();
-    } else if constexpr (FN == 7) {  // prod(cos(x * inv)) left to right
-      if (k == 0) {
-#pragma unroll
-        for (int g = 0; g < M; ++g) {
-          if (8 * g >= D) break;
-          T v[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) v[u] = (8 * g + u < D) ? row[8 * g + u] : (T)1;  // x*1 == x
-#pragma unroll
-          for (int u = 0; u < 8; ++u) prod = N::mul(prod, v[u]);
-        }
-      }
-      prod = __shfl_sync(0xffffffffu, prod, seg);
     }
   }
 
