@@ -224,6 +224,15 @@ int psso_solve(const psso_config* cfg, int64_t niter, double* traj, void* best_p
 int psso_solve_batch(const psso_config* cfg, const uint64_t* seeds, int32_t nseeds, int64_t niter,
                      double* traj, void* best_position, double* best_fitness, double* wall_s);
 
+/* replaces: one run_sequential per seed (harness.py:148-163 with
+ * ScheduleKind.SEQUENTIAL) as ONE device job: nseeds swarms of cfg initialized
+ * together, then the sequential loop of all of them in one k_seq launch (one
+ * CTA per swarm).  Per swarm bit-identical to run_sequential with that seed.
+ * Same buffers, limits and errors as psso_solve_batch. */
+int psso_solve_sequential_batch(const psso_config* cfg, const uint64_t* seeds, int32_t nseeds,
+                                int64_t niter, double* traj, void* best_position,
+                                double* best_fitness, double* wall_s);
+
 #ifdef __cplusplus
 }
 #endif

@@ -35,6 +35,7 @@ EXPORTS = (
     "psso_kernel_name", "psso_solve_batch", "psso_p2p_buffer_bytes", "psso_p2p_alloc",
     "psso_p2p_free", "psso_p2p_handle", "psso_p2p_open", "psso_p2p_close", "psso_publish_p2p",
     "psso_apply_p2p", "psso_run_sequential", "psso_sequential_passes",
+    "psso_solve_sequential_batch",
 )
 
 
@@ -120,6 +121,7 @@ def load():
     L.psso_eval_rows.argtypes = [i32, i32, i64, vp, i64, vp, dbl, vp]
     L.psso_solve.argtypes = [cfgp, i64, vp, vp, ctypes.POINTER(dbl), ctypes.POINTER(dbl)]
     L.psso_solve_batch.argtypes = [cfgp, vp, i32, i64, vp, vp, vp, ctypes.POINTER(dbl)]
+    L.psso_solve_sequential_batch.argtypes = L.psso_solve_batch.argtypes
     L.psso_kernel_name.argtypes = [vp]
     L.psso_kernel_name.restype = ctypes.c_char_p
     L.psso_p2p_buffer_bytes.argtypes = [cfgp, i32]

@@ -1148,6 +1148,26 @@ int psso_run(psso_ctx* c, int64_t t0, int64_t niter) {
   return PSSO_OK;
 }
 
+// k_seq launch for B swarms stacked along the row axis (psso_seq.cuh layout).
+static cudaError_t launch_seq(psso_ctx* c, const void* f, int M, const SeqParams& q, int64_t B,
+                              cudaStream_t s) {
+  const psso_config* cfg = &c->cfg;
+  const int es = cfg->dtype == PSSO_F64 ? 8 : 4;
+  const int nw = PSSO_SEQ_NT / 32;
+  const bool smem_fn = cfg->fn_id == 3 || cfg->fn_id == 7 || cfg->fn_id == 8;
+  TileParams p = tile_params(c, M_SOLF, q.t0, nullptr, false);
+  p.off_red = (int)align16((size_t)8 * M * es);
+  p.off_bar = (int)align16((size_t)p.off_red + 16 * nw + 64 * M);
+  p.off_scr = (int)align16((size_t)p.off_bar + 8 * (nw + 1));
+  const size_t smem = (size_t)p.off_scr + (smem_fn ? (size_t)nw * 4 * (8 * M) * es : 0);
+  cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  void* args[] = {(void*)&p, (void*)&q};
+  e = cudaLaunchKernel(f, dim3(1, (unsigned)B), dim3(PSSO_SEQ_NT), args, smem, s);
+  if (e == cudaSuccess) c->launches++;
+  return e;
+}
+
 // run_sequential (core.py:213-258): one k_seq launch for the whole loop
 // (speculative passes with rollback, psso_seq.cuh).
 int psso_run_sequential(psso_ctx* c, int64_t t0, int64_t niter) {
@@ -1161,8 +1181,6 @@ int psso_run_sequential(psso_ctx* c, int64_t t0, int64_t niter) {
   const int64_t rows = cfg->nsol, D = cfg->nvar;
   const int M = D <= 32 ? 4 : D <= 64 ? 8 : 16;
   const int es = cfg->dtype == PSSO_F64 ? 8 : 4;
-  const int nw = PSSO_SEQ_NT / 32;
-  const bool smem_fn = cfg->fn_id == 3 || cfg->fn_id == 7 || cfg->fn_id == 8;
   const void* f = seq_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, M);
   if (!f) return fail(c, PSSO_E_UNSUPPORTED, "no sequential kernel for this configuration");
   if (!c->seq_xn) {
@@ -1176,12 +1194,6 @@ int psso_run_sequential(psso_ctx* c, int64_t t0, int64_t niter) {
     CK(c, cudaMemset(c->seq_passes, 0, sizeof(int64_t)));
   }
   if (niter == 0) return PSSO_OK;
-  TileParams p = tile_params(c, M_SOLF, t0, nullptr, false);
-  p.off_red = (int)align16((size_t)8 * M * es);
-  p.off_bar = (int)align16((size_t)p.off_red + 16 * nw + 64 * M);
-  p.off_scr = (int)align16((size_t)p.off_bar + 8 * (nw + 1));
-  const size_t smem = (size_t)p.off_scr + (smem_fn ? (size_t)nw * 4 * (8 * M) * es : 0);
-  CK(c, cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   SeqParams q;
   std::memset(&q, 0, sizeof q);
   q.t0 = t0;
@@ -1198,9 +1210,7 @@ int psso_run_sequential(psso_ctx* c, int64_t t0, int64_t niter) {
   q.sol_f = c->buf.sol_f;
   q.bad = c->bad;
   q.passes = c->seq_passes;
-  void* args[] = {(void*)&p, (void*)&q};
-  CK(c, cudaLaunchKernel(f, dim3(1, 1), dim3(PSSO_SEQ_NT), args, smem, c->stream));
-  c->launches++;
+  CK(c, launch_seq(c, f, M, q, 1, c->stream));
   return PSSO_OK;
 }
 
@@ -1518,8 +1528,14 @@ int psso_solve(const psso_config* cfg, int64_t niter, double* traj, void* best_p
   return PSSO_OK;
 }
 
-int psso_solve_batch(const psso_config* cfg, const uint64_t* seeds, int32_t nseeds, int64_t niter,
-                     double* traj, void* best_position, double* best_fitness, double* wall_s) {
+}  // extern "C"
+
+// Many swarms of cfg (one per seed), initialized together by the whole-run
+// kernel (do_init), then the loop of the parallel schedule (k_swarm) or of the
+// sequential schedule (k_seq, one CTA per swarm) -- one launch for all seeds.
+static int solve_batch(const psso_config* cfg, const uint64_t* seeds, int32_t nseeds, int64_t niter,
+                       double* traj, void* best_position, double* best_fitness, double* wall_s,
+                       bool sequential) {
   std::string err;
   int rc = validate(cfg, err);
   if (rc) return fail(nullptr, rc, err);
@@ -1542,11 +1558,11 @@ int psso_solve_batch(const psso_config* cfg, const uint64_t* seeds, int32_t nsee
                             : fail(nullptr, PSSO_E_UNSUPPORTED, "no whole-run kernel for this batch");
   }
   const int G = pl.G;
-  struct Buf { void* p = nullptr; } X, P, pf, gb, gf, tr, ep, sf, si, sn, sr, sd, bad;
+  struct Buf { void* p = nullptr; } X, P, pf, gb, gf, tr, ep, sf, si, sn, sr, sd, bad, xn, fn, pfn;
   cudaStream_t s = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   auto cleanup = [&]() {
-    for (Buf* b : {&X, &P, &pf, &gb, &gf, &tr, &ep, &sf, &si, &sn, &sr, &sd, &bad})
+    for (Buf* b : {&X, &P, &pf, &gb, &gf, &tr, &ep, &sf, &si, &sn, &sr, &sd, &bad, &xn, &fn, &pfn})
       if (b->p) cudaFreeAsync(b->p, s);
     if (e0) cudaEventDestroy(e0);
     if (e1) cudaEventDestroy(e1);
@@ -1612,9 +1628,41 @@ int psso_solve_batch(const psso_config* cfg, const uint64_t* seeds, int32_t nsee
   sp.do_init = 0;
   sp.t0 = 0;
   sp.niter = niter;
-  cudaEventRecord(e0, s);
-  if ((e = launch()) != cudaSuccess) { cleanup(); return cuda_fail(nullptr, e, "psso_solve_batch run"); }
-  cudaEventRecord(e1, s);
+  if (sequential) {  // speculative-pass scratch of k_seq, then its loop
+    const int M = D <= 32 ? 4 : D <= 64 ? 8 : 16;
+    const void* f = seq_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, M);
+    if (!f) { cleanup(); return fail(nullptr, PSSO_E_UNSUPPORTED, "no sequential kernel for this configuration"); }
+    if ((e = pool_alloc(&xn.p, B * N * D * es, s)) != cudaSuccess ||
+        (e = pool_alloc(&fn.p, B * N * 8, s)) != cudaSuccess ||
+        (e = pool_alloc(&pfn.p, B * N * 8, s)) != cudaSuccess) {
+      cleanup();
+      return cuda_fail(nullptr, e, "psso_solve_sequential_batch alloc");
+    }
+    SeqParams q;
+    std::memset(&q, 0, sizeof q);
+    q.t0 = 0;
+    q.niter = niter;
+    q.rows = (int64_t)N;
+    q.Xn = xn.p;
+    q.fn = (double*)fn.p;
+    q.pfn = (double*)pfn.p;
+    q.traj = (double*)tr.p;
+    q.traj_stride = niter;
+    q.g_f = (double*)gf.p;
+    q.gbest = gb.p;
+    q.seeds = (const uint64_t*)sd.p;
+    q.bad = (unsigned long long*)bad.p;
+    cudaEventRecord(e0, s);
+    if ((e = launch_seq(c, f, M, q, (int64_t)B, s)) != cudaSuccess) {
+      cleanup();
+      return cuda_fail(nullptr, e, "psso_solve_sequential_batch run");
+    }
+    cudaEventRecord(e1, s);
+  } else {
+    cudaEventRecord(e0, s);
+    if ((e = launch()) != cudaSuccess) { cleanup(); return cuda_fail(nullptr, e, "psso_solve_batch run"); }
+    cudaEventRecord(e1, s);
+  }
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) { cleanup(); return cuda_fail(nullptr, e, "psso_solve_batch"); }
   std::vector<unsigned long long> bk(B);
   e = cudaMemcpy(bk.data(), bad.p, B * 8, cudaMemcpyDeviceToHost);
@@ -1636,6 +1684,19 @@ int psso_solve_batch(const psso_config* cfg, const uint64_t* seeds, int32_t nsee
   cleanup();
   if (e != cudaSuccess) return cuda_fail(nullptr, e, "psso_solve_batch copy-back");
   return PSSO_OK;
+}
+
+extern "C" {
+
+int psso_solve_batch(const psso_config* cfg, const uint64_t* seeds, int32_t nseeds, int64_t niter,
+                     double* traj, void* best_position, double* best_fitness, double* wall_s) {
+  return solve_batch(cfg, seeds, nseeds, niter, traj, best_position, best_fitness, wall_s, false);
+}
+
+int psso_solve_sequential_batch(const psso_config* cfg, const uint64_t* seeds, int32_t nseeds,
+                                int64_t niter, double* traj, void* best_position,
+                                double* best_fitness, double* wall_s) {
+  return solve_batch(cfg, seeds, nseeds, niter, traj, best_position, best_fitness, wall_s, true);
 }
 
 }  // extern "C"

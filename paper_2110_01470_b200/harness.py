@@ -10,10 +10,11 @@ side by side in the whole-run kernel (``run_parallel_batch``), and the records
 reference's CSV schema and formatting, so the reference's readers, summaries,
 statistics and plotting tools consume them unchanged.
 
-Only the parallel schedule is provided: the sequential-asynchronous schedule
-is serial across particles by definition and stays in the
-reference.  Shapes the batched kernel does not take (nvar > 128, or
-nsol*nvar > 2^22) fall back to one ``run_parallel`` per seed on the device.
+Both schedules run on the device: a sequential cell is likewise ONE job
+(``run_sequential_batch``: one k_seq launch, one CTA per seed), bit-identical
+per seed to the reference's ``run_sequential``.  Shapes the batched kernels
+do not take (nvar > 128, or nsol*nvar > 2^22) fall back to one device run per
+seed (the parallel schedule; the sequential one needs nvar <= 128).
 """
 
 from __future__ import annotations
@@ -26,7 +27,8 @@ import numpy as np
 
 from .benchmarks import BenchmarkFn, make_function
 from .core import SsoParams
-from .parallel import LayoutMode, run_parallel, run_parallel_batch
+from .core import run_sequential
+from .parallel import LayoutMode, run_parallel, run_parallel_batch, run_sequential_batch
 from .records import RunRecord, ScheduleKind
 
 __all__ = [
@@ -82,7 +84,7 @@ class SpeedupReport:
 
 @dataclass
 class ExperimentConfig:
-    """The reference's experiment configuration (harness.py:96-128), parallel schedule.
+    """The reference's experiment configuration (harness.py:96-128).
 
     Extra keyword fields: ``dtype`` and ``rng`` as in ``run_parallel``.
     ``workers``, ``layout`` and ``block_size`` are accepted and have no effect
@@ -112,9 +114,6 @@ class ExperimentConfig:
         if not self.schedules:
             raise ValueError("config key 'schedules' must list at least one schedule")
         self.schedules = [ScheduleKind(s) for s in self.schedules]
-        if ScheduleKind.SEQUENTIAL in self.schedules:
-            raise ValueError("the sequential schedule is not provided by the B200 engine "
-                             "(serial across particles); run it with the reference")
         self.layout = LayoutMode(self.layout)
         if not 0.0 <= self.cw <= self.cp <= self.cg <= 1.0:
             raise ValueError(
@@ -138,8 +137,9 @@ def _function(entry, nvar: int) -> BenchmarkFn:
     return entry if isinstance(entry, BenchmarkFn) else make_function(entry, nvar)
 
 
-def run_cell(fn: BenchmarkFn, config: ExperimentConfig, run_ids: Sequence[int]) -> list:
-    """Replications ``run_ids`` of one parallel cell (reference _run_one, harness.py:148-163).
+def run_cell(fn: BenchmarkFn, config: ExperimentConfig, run_ids: Sequence[int],
+             schedule: ScheduleKind = ScheduleKind.PARALLEL) -> list:
+    """Replications ``run_ids`` of one cell (reference _run_one, harness.py:148-163).
 
     Seeds are ``base_seed + run_id``.  One batched launch when the shape allows
     it; ``wall_time_s`` is then the batch's loop time divided evenly over its
@@ -149,10 +149,15 @@ def run_cell(fn: BenchmarkFn, config: ExperimentConfig, run_ids: Sequence[int]) 
                        var_max=fn.var_max, nsol=config.nsol, nvar=config.nvar,
                        niter=config.niter)
     seeds = [config.base_seed + rid for rid in run_ids]
+    sequential = ScheduleKind(schedule) is ScheduleKind.SEQUENTIAL
     if config.nvar <= 128 and config.nsol * config.nvar <= _BATCH_MAX_ELEMS:
-        recs = run_parallel_batch(params, fn, seeds, dtype=config.dtype, rng=config.rng)
+        batch = run_sequential_batch if sequential else run_parallel_batch
+        recs = batch(params, fn, seeds, dtype=config.dtype, rng=config.rng)
         per_run = recs[0].wall_time_s / len(recs)
         recs = [replace(r, run_id=rid, wall_time_s=per_run) for r, rid in zip(recs, run_ids)]
+    elif sequential:
+        recs = [replace(run_sequential(params, fn, s, dtype=config.dtype, rng=config.rng), run_id=rid)
+                for s, rid in zip(seeds, run_ids)]
     else:
         recs = [replace(run_parallel(params, fn, s, workers=config.workers, layout=config.layout,
                                      dtype=config.dtype, rng=config.rng), run_id=rid)
@@ -218,8 +223,8 @@ def run_experiment(config: ExperimentConfig, out=None, summary_out=None) -> Expe
     records = []
     try:
         for fn in functions:
-            for _schedule in config.schedules:  # parallel only (validated)
-                for rec in run_cell(fn, config, range(config.replications)):
+            for schedule in config.schedules:
+                for rec in run_cell(fn, config, range(config.replications), schedule):
                     sink.add(rec)
                     records.append(rec)
     except BaseException as exc:

@@ -34,6 +34,7 @@ __all__ = [
     "update_gbest_phase",
     "run_parallel",
     "run_parallel_batch",
+    "run_sequential_batch",
 ]
 
 
@@ -228,6 +229,30 @@ def run_parallel_batch(
     ``wall_time_s`` is the loop-only device time of the whole batch.  Needs
     ``nvar <= 128`` and ``nsol * nvar <= 2**22``.
     """
+    return _solve_batch(params, f, seeds, dtype, rng, run_id_base, sequential=False)
+
+
+def run_sequential_batch(
+    params: SsoParams,
+    f,
+    seeds,
+    *,
+    dtype: str = "float64",
+    rng: str = "reference",
+    run_id_base: int = 0,
+) -> list:
+    """Many independent runs of ``run_sequential`` (core.py:213-258) as one device job.
+
+    All swarms are initialized together and their sequential loops run in one
+    k_seq launch, one CTA per swarm (psso_solve_sequential_batch).  Record k is
+    bit-identical to ``run_sequential(params, f, seeds[k])``; ``wall_time_s``
+    is the loop-only device time of the whole batch.  Same limits as
+    ``run_parallel_batch``.
+    """
+    return _solve_batch(params, f, seeds, dtype, rng, run_id_base, sequential=True)
+
+
+def _solve_batch(params, f, seeds, dtype, rng, run_id_base, sequential) -> list:
     import ctypes
 
     from . import _lib
@@ -246,8 +271,9 @@ def run_parallel_batch(
     best = np.empty((B, D), dtype=np.float64 if dtype == "float64" else np.float32)
     bestf = np.empty(B, dtype=np.float64)
     wall = ctypes.c_double()
-    rc = L.psso_solve_batch(ctypes.byref(cfg), arr, B, n, traj.ctypes.data, best.ctypes.data,
-                            bestf.ctypes.data, ctypes.byref(wall))
+    solve = L.psso_solve_sequential_batch if sequential else L.psso_solve_batch
+    rc = solve(ctypes.byref(cfg), arr, B, n, traj.ctypes.data, best.ctypes.data,
+               bestf.ctypes.data, ctypes.byref(wall))
     if rc == _lib.PSSO_E_NONFINITE:  # "... at particle I (during initialization | at iteration T)"
         import re
 
@@ -256,8 +282,9 @@ def run_parallel_batch(
         it = None if m is None or m.group(2) is None else int(m.group(2))
         raise NonFiniteFitnessError(float("nan"), int(m.group(1)) if m else -1, it)
     _lib.check(rc)
+    kind = ScheduleKind.SEQUENTIAL if sequential else ScheduleKind.PARALLEL
     return [
-        RunRecord(run_id=run_id_base + k, schedule=ScheduleKind.PARALLEL,
+        RunRecord(run_id=run_id_base + k, schedule=kind,
                   function=getattr(f, "id", "custom"), nsol=params.nsol, nvar=D, niter=n,
                   cw=params.cw, cp=params.cp, cg=params.cg, seed=seeds[k],
                   best_fitness=float(bestf[k]), wall_time_s=wall.value,

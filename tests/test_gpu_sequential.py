@@ -177,3 +177,27 @@ def test_sequential_fp32_and_philox_modes_run():
         assert np.all(np.abs(rec.best_position) <= 5.12)
         assert rec.best_fitness == pytest.approx(fn(rec.best_position[None, :].astype(np.float64))[0],
                                                  rel=1e-5)
+
+
+@pytest.mark.parametrize("fid,nsol,nvar,niter,nseeds", [
+    ("f1", 100, 30, 200, 5), ("f4", 64, 64, 50, 3), ("f7", 40, 100, 30, 4), ("f5", 300, 128, 20, 2),
+])
+def test_sequential_batch_equals_single_runs(fid, nsol, nvar, niter, nseeds):
+    fn = _fn(fid, nvar)
+    p = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=fn.var_min, var_max=fn.var_max,
+                       nsol=nsol, nvar=nvar, niter=niter)
+    seeds = [3 + 7 * k for k in range(nseeds)]
+    recs = psso.run_sequential_batch(p, fn, seeds)
+    for rec, s in zip(recs, seeds):
+        one = psso.run_sequential(p, fn, s)
+        assert rec.schedule == psso.ScheduleKind.SEQUENTIAL and rec.seed == s
+        assert np.array_equal(rec.best_position, one.best_position)
+        assert np.array_equal(rec.trajectory, one.trajectory)
+
+
+def test_sequential_batch_c1_appendix_value():
+    fn = psso.make_function("f1", 30)
+    p = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=-5.12, var_max=5.12, nsol=100, nvar=30,
+                       niter=1000)
+    recs = psso.run_sequential_batch(p, fn, [1, 0])
+    assert recs[1].best_fitness == 10.383304882651581

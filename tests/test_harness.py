@@ -18,10 +18,15 @@ CELLS = dict(functions=["f1", "f4", "f5", "f7"], schedules=[ScheduleKind.PARALLE
              replications=4, base_seed=7, nsol=64, nvar=16, niter=60)
 
 
-def _golden_records(tmp_path):
-    text = (GOLD / "harness_records.csv").read_text().splitlines()
+SEQ_CELLS = dict(functions=["f1", "f4", "f6"],
+                 schedules=[ScheduleKind.SEQUENTIAL, ScheduleKind.PARALLEL],
+                 replications=3, base_seed=11, nsol=48, nvar=20, niter=40)
+
+
+def _golden_records(tmp_path, stem="harness"):
+    text = (GOLD / f"{stem}_records.csv").read_text().splitlines()
     filled = [text[0]] + [r + "0.0" for r in text[1:]]  # wall time is machine-dependent
-    p = tmp_path / "g.csv"
+    p = tmp_path / f"{stem}_g.csv"
     p.write_text("\n".join(filled) + "\n")
     return H.read_records(p)
 
@@ -51,8 +56,10 @@ def test_speedup_arithmetic_table_a3():
 
 
 def test_config_validation():
-    with pytest.raises(ValueError, match="sequential"):
-        H.ExperimentConfig(schedules=[ScheduleKind.SEQUENTIAL])
+    assert H.ExperimentConfig(schedules=["sequential", "parallel"]).schedules == [
+        ScheduleKind.SEQUENTIAL, ScheduleKind.PARALLEL]
+    with pytest.raises(ValueError, match="schedules"):
+        H.ExperimentConfig(schedules=[])
     with pytest.raises(ValueError, match="thresholds"):
         H.ExperimentConfig(cw=0.5, cp=0.4)
     with pytest.raises(ValueError, match="replications"):
@@ -77,3 +84,30 @@ def test_run_experiment_matches_reference_rows(tmp_path):
         else:                            # transcendental objectives: 1e-12
             assert abs(a.best_fitness - b.best_fitness) <= 1e-12 * abs(b.best_fitness)
         assert a.wall_time_s > 0
+
+
+def test_sequential_golden_summary_round_trip(tmp_path):
+    recs = _golden_records(tmp_path, "harness_seq")
+    assert [r.schedule for r in recs[:4]] == [ScheduleKind.SEQUENTIAL] * 3 + [ScheduleKind.PARALLEL]
+    s = tmp_path / "s.csv"
+    H.write_summary(H.summarize(recs), s)
+    assert s.read_text() == (GOLD / "harness_seq_summary.csv").read_text()
+
+
+@pytest.mark.gpu
+def test_run_experiment_both_schedules_match_reference_rows(tmp_path):
+    """Sequential and parallel cells on device == the reference harness's rows."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    out = tmp_path / "r.csv"
+    H.run_experiment(H.ExperimentConfig(**SEQ_CELLS), out=out)
+    gold = _golden_records(tmp_path, "harness_seq")
+    mine = H.read_records(out)
+    assert len(mine) == len(gold) == 18
+    for a, b in zip(mine, gold):
+        assert (a.run_id, a.schedule, a.function, a.seed) == (b.run_id, b.schedule, b.function, b.seed)
+        if a.function in ("f1", "f4"):
+            assert a.best_fitness == b.best_fitness
+        else:
+            assert abs(a.best_fitness - b.best_fitness) <= 1e-12 * abs(b.best_fitness)
