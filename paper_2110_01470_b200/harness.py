@@ -33,6 +33,11 @@ from .records import RunRecord, ScheduleKind
 
 __all__ = [
     "CSV_HEADER",
+    "DEFAULT_TRIPLES",
+    "SweepConfig",
+    "SweepReport",
+    "parameter_sweep",
+    "write_trajectories",
     "ExperimentConfig",
     "ExperimentReport",
     "SpeedupReport",
@@ -45,6 +50,19 @@ __all__ = [
     "write_records",
     "write_summary",
 ]
+
+#: reference defaults (harness.py:49-68): the paper's setup
+DEFAULT_TRIPLES = ((0.1, 0.3, 0.7), (0.1, 0.4, 0.8), (0.2, 0.4, 0.6), (0.2, 0.5, 0.9),
+                   (0.3, 0.4, 0.5), (0.3, 0.6, 0.8))
+DEFAULT_NSOL = 100
+DEFAULT_NVAR = 50
+DEFAULT_NITER = 1000
+DEFAULT_THRESHOLDS = (0.3, 0.6, 0.8)
+DEFAULT_REPLICATIONS = 20
+DEFAULT_POWER_A = 84.0
+DEFAULT_POWER_B = 180.0
+#: trajectory sidecar header (harness.py:318)
+TRAJECTORY_HEADER = "# columns: run_id schedule function iteration gbest_fitness"
 
 #: results CSV columns, identical to the reference (harness.py:46)
 CSV_HEADER = "run_id,schedule,function,nsol,nvar,niter,cw,cp,cg,seed,best_fitness,wall_time_s"
@@ -295,3 +313,67 @@ def compute_speedup(times_a, times_b, power_a: float, power_b: float,
     return SpeedupReport(mean_time_a=ma, mean_time_b=mb, speedup=s, power_a=power_a,
                          power_b=power_b, power_ratio=ratio, rectified_efficiency=s / ratio,
                          nsol=nsol)
+
+
+def write_trajectories(records: Sequence[RunRecord], path) -> None:
+    """Sidecar with the per-iteration gBest curve of each run (reference harness.py:321-336)."""
+    with open(path, "w", encoding="utf-8") as fh:
+        fh.write(TRAJECTORY_HEADER + "\n")
+        for rec in records:
+            if rec.trajectory is None:
+                continue
+            for t, value in enumerate(rec.trajectory):
+                fh.write(f"{rec.run_id} {rec.schedule} {rec.function} {t} {float(value)!r}\n")
+
+
+@dataclass
+class SweepConfig:
+    """Threshold sweep (reference harness.py:388-398)."""
+
+    function: Union[str, BenchmarkFn] = "f1"
+    triples: Sequence[tuple] = DEFAULT_TRIPLES
+    replications: int = DEFAULT_REPLICATIONS
+    base_seed: int = 0
+    nsol: int = DEFAULT_NSOL
+    nvar: int = DEFAULT_NVAR
+    niter: int = DEFAULT_NITER
+    workers: int = 1
+    schedule: ScheduleKind = ScheduleKind.PARALLEL
+    dtype: str = "float64"
+    rng: str = "reference"
+
+
+@dataclass
+class SweepReport:
+    config: SweepConfig
+    records: list
+    groups: dict
+    summaries: list
+    note: Optional[str] = None
+
+
+def parameter_sweep(config: SweepConfig) -> SweepReport:
+    """Every threshold triple as one device cell (reference harness.py:410-444).
+
+    The between-group Kruskal-Wallis test of the reference is statistics on
+    the records, outside the hot path: the records CSV written from
+    ``SweepReport.records`` has the reference schema, so the reference's
+    ``sso stats --test kruskal --group-by cw,cp,cg`` runs on it unchanged.
+    """
+    fn = _function(config.function, config.nvar)
+    for triple in config.triples:  # reject malformed triples before any compute
+        SsoParams(cw=triple[0], cp=triple[1], cg=triple[2], var_min=fn.var_min,
+                  var_max=fn.var_max, nsol=config.nsol, nvar=config.nvar, niter=config.niter)
+    records, groups = [], {}
+    for triple in config.triples:
+        cell = ExperimentConfig(functions=[fn], schedules=[config.schedule],
+                                replications=config.replications, base_seed=config.base_seed,
+                                nsol=config.nsol, nvar=config.nvar, niter=config.niter,
+                                cw=triple[0], cp=triple[1], cg=triple[2], workers=config.workers,
+                                dtype=config.dtype, rng=config.rng)
+        cell_records = run_experiment(cell).records
+        records.extend(cell_records)
+        groups[tuple(triple)] = [r.best_fitness for r in cell_records]
+    note = ("only one combination swept; no between-group comparison" if len(groups) < 2 else
+            "between-group test: reference `sso stats --test kruskal --group-by cw,cp,cg` on the records")
+    return SweepReport(config, records, groups, summarize(records), note=note)
