@@ -1148,22 +1148,45 @@ int psso_run(psso_ctx* c, int64_t t0, int64_t niter) {
   return PSSO_OK;
 }
 
-// k_seq launch for B swarms stacked along the row axis (psso_seq.cuh layout).
-static cudaError_t launch_seq(psso_ctx* c, const void* f, int M, const SeqParams& q, int64_t B,
+// k_seq launch for B swarms stacked along the row axis (psso_seq.cuh layout):
+// one cluster of G CTAs per swarm, G = ceil(rows / 64) up to 16 (about one
+// row group per warp) -- one CTA up to 128 rows, where the cluster barrier
+// costs more than it saves (C1: 5.7 vs 6.2 ms); PSSO_SEQ_G overrides.  Rows
+// are split in blocks of rpc.
+static cudaError_t launch_seq(psso_ctx* c, const void* f, int M, SeqParams q, int64_t B,
                               cudaStream_t s) {
   const psso_config* cfg = &c->cfg;
   const int es = cfg->dtype == PSSO_F64 ? 8 : 4;
   const int nw = PSSO_SEQ_NT / 32;
   const bool smem_fn = cfg->fn_id == 3 || cfg->fn_id == 7 || cfg->fn_id == 8;
+  int64_t G = q.rows <= 128 ? 1 : std::min<int64_t>(16, (q.rows + 63) / 64);
+  if (const char* g = std::getenv("PSSO_SEQ_G"))
+    if (*g) G = std::max<int64_t>(1, std::min<int64_t>(16, std::atoll(g)));
+  q.rpc = ((q.rows + G - 1) / G + 3) / 4 * 4;
+  G = (q.rows + q.rpc - 1) / q.rpc;
   TileParams p = tile_params(c, M_SOLF, q.t0, nullptr, false);
   p.off_red = (int)align16((size_t)8 * M * es);
   p.off_bar = (int)align16((size_t)p.off_red + 16 * nw + 64 * M);
-  p.off_scr = (int)align16((size_t)p.off_bar + 8 * (nw + 1));
-  const size_t smem = (size_t)p.off_scr + (smem_fn ? (size_t)nw * 4 * (8 * M) * es : 0);
+  p.off_scr = (int)align16((size_t)p.off_bar + 8 * (nw + 2));
+  p.off_leaf = (int)align16((size_t)p.off_scr + (smem_fn ? (size_t)nw * 4 * (8 * M) * es : 0));
+  const size_t smem = (size_t)p.off_leaf + 32 + 2 * (size_t)cfg->nvar * es;
   cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess && G > 8) e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t lc = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)G;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.gridDim = dim3((unsigned)G, (unsigned)B, 1);
+  lc.blockDim = dim3(PSSO_SEQ_NT, 1, 1);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = s;
+  lc.attrs = at;
+  lc.numAttrs = 1;
   void* args[] = {(void*)&p, (void*)&q};
-  e = cudaLaunchKernel(f, dim3(1, (unsigned)B), dim3(PSSO_SEQ_NT), args, smem, s);
+  e = cudaLaunchKernelExC(&lc, f, args);
   if (e == cudaSuccess) c->launches++;
   return e;
 }

@@ -19,10 +19,17 @@
 //   gbest move of r* is applied; the next pass starts at r* + 1.
 //
 // An iteration costs 1 + (gbest moves in it) passes; the results are
-// bit-identical to the serial loop.  One CTA per swarm (blockIdx.y = swarm of
-// a batch), the swarm's rows in global memory (L2-resident at the sizes this
-// schedule is used at), gbest in shared memory.
+// bit-identical to the serial loop.  One thread-block cluster of G <= 16
+// CTAs per swarm (blockIdx.y = swarm of a batch): CTA c owns a contiguous
+// block of rows; per pass each CTA finds its own first event, publishes it
+// (row index, fitness, the row itself) in its shared memory, one hardware
+// cluster barrier, and every CTA takes the lowest-index event over DSMEM --
+// records double-buffered by pass parity, so one barrier per pass suffices.
+// The swarm's rows stay in global memory (L2-resident at the sizes this
+// schedule is used at), gbest in each CTA's shared memory.
 #pragma once
+
+#include <cooperative_groups.h>
 
 #include "psso_device.cuh"
 
@@ -46,13 +53,15 @@ struct SeqParams {
   double* sol_f;            // [B][rows] or null
   unsigned long long* bad;  // [B]: min((t+1) << 40 | i) of the first non-finite fitness
   int64_t* passes;          // [B] passes run (diagnostic) or null
+  int64_t rpc;              // rows per CTA of the cluster (multiple of 4)
 };
 
 // Shared memory (offsets in TileParams):
 //   0        gbest (8M entries of T; entries past D are read and discarded)
 //   off_red  warp reduction (16 * NW) + xs30(gamma*(j+1)) table (8 * 8M)
-//   off_bar  first-event reduction: NW int64 + 1
+//   off_bar  first-event reduction: NW int64 + 2
 //   off_scr  per-warp smem rows [4][8M] (f3, f7, f8)
+//   off_leaf published event records [2][row index, fitness] + rows [2][D]
 template <typename T, int FN, int RNG, int M>
 __global__ void __launch_bounds__(PSSO_SEQ_NT, 1)
     k_seq(const __grid_constant__ TileParams p, const __grid_constant__ SeqParams q) {
@@ -61,15 +70,20 @@ __global__ void __launch_bounds__(PSSO_SEQ_NT, 1)
   extern __shared__ __align__(128) unsigned char smem[];
   T* gb = reinterpret_cast<T*>(smem);
   uint64_t* xg = reinterpret_cast<uint64_t*>(smem + p.off_red + 16 * NW);  // [8M]
-  int64_t* red = reinterpret_cast<int64_t*>(smem + p.off_bar);            // [NW + 1]
+  int64_t* red = reinterpret_cast<int64_t*>(smem + p.off_bar);            // [NW + 2]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = lane & 7;
-  const int b = blockIdx.y;
+  const int b = blockIdx.y, c = blockIdx.x, G = gridDim.x;
   const int D = p.D;
   const int64_t rows = q.rows;
-  const int64_t ngroups = (rows + 3) >> 2;
+  const int64_t r0 = (int64_t)c * q.rpc, r1 = min(rows, r0 + q.rpc);  // this CTA's rows
   T* scr = reinterpret_cast<T*>(smem + p.off_scr) + warp * 4 * (8 * M);
+  int64_t* pub_i = reinterpret_cast<int64_t*>(smem + p.off_leaf);     // [2]
+  double* pub_f = reinterpret_cast<double*>(smem + p.off_leaf + 16);  // [2]
+  T* pub_row = reinterpret_cast<T*>(smem + p.off_leaf + 32);          // [2][D]
+  namespace cgx = cooperative_groups;
+  cgx::cluster_group cluster = cgx::this_cluster();
 
   T* X = reinterpret_cast<T*>(p.X) + (int64_t)b * rows * D;
   T* P = reinterpret_cast<T*>(p.P) + (int64_t)b * rows * D;
@@ -79,7 +93,8 @@ __global__ void __launch_bounds__(PSSO_SEQ_NT, 1)
   double* sf = q.sol_f ? q.sol_f + (int64_t)b * rows : nullptr;
   T* gbp = reinterpret_cast<T*>(q.gbest) + (int64_t)b * D;
   unsigned long long* bad = q.bad + b;
-  if (*(volatile unsigned long long*)bad != ~0ull) return;  // an earlier non-finite fitness
+  // a flag raised before the launch: every CTA of the cluster sees it and leaves
+  if (*(volatile unsigned long long*)bad != ~0ull) return;
 
   // chain_step writes its row to ev.X (and, when it improves, again to ev.P),
   // its fitness to ev.sol_f and improved fitness to ev.p_f: all scratch here
@@ -104,6 +119,7 @@ __global__ void __launch_bounds__(PSSO_SEQ_NT, 1)
   }
   double gf = q.g_f[b];
   int64_t npass = 0;
+  int par = 0;
   bool stop = false;
   __syncthreads();
 
@@ -117,14 +133,15 @@ __global__ void __launch_bounds__(PSSO_SEQ_NT, 1)
     int64_t lo = 0;
     while (lo < rows) {
       ++npass;
-      // ---- speculative pass over rows [lo, rows) (core.py:227-232 for every row at once)
+      const int64_t a0 = max(lo, r0);  // this CTA's rows of the pass: [a0, r1)
+      // ---- speculative pass (core.py:227-232 for every remaining row at once)
       double best_f = CUDART_INF;
       int64_t best_i = INT64_MAX;
       int best_new = 0;
-      for (int64_t grp = (lo >> 2) + warp; grp < ngroups; grp += NW) {
+      for (int64_t grp = (a0 >> 2) + warp; 4 * grp < r1; grp += NW) {
         const int64_t r = 4 * grp + (lane >> 3);
-        const bool rv = r < rows && r >= lo;
-        const int64_t rl = r < rows ? r : rows - 1;
+        const bool rv = r < r1 && r >= a0;
+        const int64_t rl = r < r1 ? r : r1 - 1;
         const double pf_row = pf[rl];
         const T* xl = X + rl * (int64_t)D;
         const T* pl = P + rl * (int64_t)D;
@@ -138,10 +155,10 @@ __global__ void __launch_bounds__(PSSO_SEQ_NT, 1)
         chain_step<T, FN, RNG, M, false, false, true>(p, ev, gb, xg, scr, r, rv, x, pv, pf_row,
                                                       best_f, best_i, best_new);
       }
-      __syncthreads();  // Xn / fn of the pass visible to the block
-      // ---- first event r* >= lo: non-finite (core.py:233) or a gbest move (core.py:236-241)
+      __syncthreads();  // Xn / fn of the pass visible to the CTA
+      // ---- this CTA's first event: non-finite (core.py:233) or a gbest move (core.py:236-241)
       int64_t ev_r = INT64_MAX;
-      for (int64_t r = lo + tid; r < rows; r += NTC) {
+      for (int64_t r = a0 + tid; r < r1; r += NTC) {
         const double f = fn[r];
         if (!isfinite(f) || (f <= pf[r] && f <= gf)) { ev_r = r; break; }
       }
@@ -153,13 +170,40 @@ __global__ void __launch_bounds__(PSSO_SEQ_NT, 1)
         int64_t v = lane < NW ? red[lane] : INT64_MAX;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
-        if (lane == 0) red[NW] = v;
+        if (lane == 0) {
+          pub_i[par] = v;
+          pub_f[par] = v != INT64_MAX ? fn[v] : 0.0;
+          red[NW] = v;
+        }
+      }
+      __syncthreads();
+      {  // publish the event row (read by every CTA after the barrier)
+        const int64_t v = red[NW];
+        if (v != INT64_MAX)
+          for (int j = tid; j < D; j += NTC) pub_row[par * D + j] = Xn[v * (int64_t)D + j];
+      }
+      cluster.sync();  // every CTA's record of this pass is published
+      if (warp == 0) {  // lowest-index event over the cluster (DSMEM)
+        int64_t v = INT64_MAX;
+        int own = 0;
+        if (lane < G) {
+          v = cluster.map_shared_rank(pub_i, lane)[par];
+          own = lane;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const int64_t ov = __shfl_xor_sync(0xffffffffu, v, o);
+          const int oo = __shfl_xor_sync(0xffffffffu, own, o);
+          if (ov < v) { v = ov; own = oo; }
+        }
+        if (lane == 0) { red[NW] = v; red[NW + 1] = own; }
       }
       __syncthreads();
       const int64_t rs = red[NW];
-      const int64_t hi = rs < rows ? rs : rows - 1;  // last committed row
-      // ---- commit rows lo..hi: X always (core.py:231), pBest on `<=` (core.py:236-238)
-      for (int64_t r = lo + warp; r <= hi; r += NW) {
+      const int own = (int)red[NW + 1];
+      const int64_t hi = min(rs, r1 - 1);  // last committed row of this CTA
+      // ---- commit this CTA's rows a0..hi: X always (core.py:231), pBest on `<=` (:236-238)
+      for (int64_t r = a0 + warp; r <= hi; r += NW) {
         const double f = fn[r];
         const bool imp = isfinite(f) && f <= pf[r];
         const T* src = Xn + r * (int64_t)D;
@@ -170,32 +214,37 @@ __global__ void __launch_bounds__(PSSO_SEQ_NT, 1)
         }
       }
       __syncthreads();  // pBest rows copied before p_f moves
-      for (int64_t r = lo + tid; r <= hi; r += NTC) {
+      for (int64_t r = a0 + tid; r <= hi; r += NTC) {
         const double f = fn[r];
         if (sf) sf[r] = f;
         if (isfinite(f) && f <= pf[r]) pf[r] = f;
       }
-      if (rs < rows) {
-        const double f = fn[rs];
+      if (rs != INT64_MAX) {
+        const double f = cluster.map_shared_rank(pub_f, own)[par];
         if (!isfinite(f)) {
-          if (tid == 0) *bad = ((unsigned long long)(t + 1) << 40) | (unsigned long long)rs;
+          if (c == 0 && tid == 0) *bad = ((unsigned long long)(t + 1) << 40) | (unsigned long long)rs;
           stop = true;
         } else {  // gbest <- pbests[r*] (core.py:239-241)
-          for (int j = tid; j < D; j += NTC) gb[j] = Xn[rs * (int64_t)D + j];
+          const T* src = cluster.map_shared_rank(pub_row, own) + par * D;
+          for (int j = tid; j < D; j += NTC) gb[j] = src[j];
           gf = f;
         }
       }
       __syncthreads();
+      par ^= 1;
       if (stop) break;
-      lo = rs < rows ? rs + 1 : rows;
+      lo = rs != INT64_MAX ? rs + 1 : rows;
     }
-    if (!stop && tid == 0 && q.traj) q.traj[b * q.traj_stride + t] = gf;  // core.py:242
+    if (!stop && c == 0 && tid == 0 && q.traj) q.traj[b * q.traj_stride + t] = gf;  // core.py:242
   }
-  for (int j = tid; j < D; j += NTC) gbp[j] = gb[j];
-  if (tid == 0) {
-    q.g_f[b] = gf;
-    if (q.passes) q.passes[b] = npass;
+  if (c == 0) {
+    for (int j = tid; j < D; j += NTC) gbp[j] = gb[j];
+    if (tid == 0) {
+      q.g_f[b] = gf;
+      if (q.passes) q.passes[b] = npass;
+    }
   }
+  cluster.sync();  // no CTA leaves while its shared memory may still be read
 }
 
 }  // namespace psso
