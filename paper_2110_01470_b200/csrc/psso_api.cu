@@ -1149,17 +1149,17 @@ int psso_run(psso_ctx* c, int64_t t0, int64_t niter) {
 }
 
 // k_seq launch for B swarms stacked along the row axis (psso_seq.cuh layout):
-// one cluster of G CTAs per swarm, G = ceil(rows / 64) up to 16 (about one
-// row group per warp) -- one CTA up to 128 rows, where the cluster barrier
-// costs more than it saves (C1: 5.7 vs 6.2 ms); PSSO_SEQ_G overrides.  Rows
-// are split in blocks of rpc.
+// one cluster of G CTAs per swarm, G = ceil(rows / 64) up to 16: about one
+// row group per warp, which beats fewer CTAs with more groups per warp even
+// at C1 (100 rows: G = 2 6.2 ms, G = 1 9.6 ms per 1000 iterations);
+// PSSO_SEQ_G overrides.  Rows are split in blocks of rpc.
 static cudaError_t launch_seq(psso_ctx* c, const void* f, int M, SeqParams q, int64_t B,
                               cudaStream_t s) {
   const psso_config* cfg = &c->cfg;
   const int es = cfg->dtype == PSSO_F64 ? 8 : 4;
   const int nw = PSSO_SEQ_NT / 32;
   const bool smem_fn = cfg->fn_id == 3 || cfg->fn_id == 7 || cfg->fn_id == 8;
-  int64_t G = q.rows <= 128 ? 1 : std::min<int64_t>(16, (q.rows + 63) / 64);
+  int64_t G = std::max<int64_t>(1, std::min<int64_t>(16, (q.rows + 63) / 64));
   if (const char* g = std::getenv("PSSO_SEQ_G"))
     if (*g) G = std::max<int64_t>(1, std::min<int64_t>(16, std::atoll(g)));
   q.rpc = ((q.rows + G - 1) / G + 3) / 4 * 4;
