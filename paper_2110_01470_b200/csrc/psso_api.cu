@@ -5,6 +5,7 @@
 // Reference anchors (/root/reference/pkg/src/sso/): run_parallel
 // parallel.py:152-233; phases parallel.py:120-144; initialize core.py:196-210;
 // RngStream.uniform rng.py:73-87; BenchmarkFn.__call__ benchmarks.py:86-94.
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -1492,6 +1493,17 @@ int psso_eval_rows(int32_t fn_id, int32_t dtype, int64_t nvar, const void* x, in
 
 int psso_solve(const psso_config* cfg, int64_t niter, double* traj, void* best_position,
                double* best_fitness, double* wall_s) {
+  // PSSO_SOLVE_TRACE=1: host time of each phase to stderr (diagnostic)
+  const char* tr_env = std::getenv("PSSO_SOLVE_TRACE");
+  const bool trace = tr_env && *tr_env && *tr_env != '0';
+  auto tp = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!trace) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[psso_solve] %-10s %9.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - tp).count());
+    tp = now;
+  };
   std::string err;
   int rc = validate(cfg, err);
   if (rc) return fail(nullptr, rc, err);
@@ -1507,11 +1519,13 @@ int psso_solve(const psso_config* cfg, int64_t niter, double* traj, void* best_p
   cudaError_t e = cudaSuccess;
   auto cleanup = [&]() {
     if (c) psso_destroy(c);
+    mark("destroy");
     for (void* q : {b.sol, b.pbests, (void*)b.p_f, b.gbest, (void*)b.g_f, (void*)b.traj})
       if (q) cudaFreeAsync(q, s);
+    mark("freeasync");
     if (e0) cudaEventDestroy(e0);
     if (e1) cudaEventDestroy(e1);
-    if (s) { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
+    if (s) { cudaStreamSynchronize(s); mark("streamsync"); cudaStreamDestroy(s); }
   };
   if ((e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) != cudaSuccess ||
       (e = cudaEventCreate(&e0)) != cudaSuccess || (e = cudaEventCreate(&e1)) != cudaSuccess ||
@@ -1524,7 +1538,9 @@ int psso_solve(const psso_config* cfg, int64_t niter, double* traj, void* best_p
     cleanup();
     return cuda_fail(nullptr, e, "psso_solve alloc");
   }
+  mark("alloc");
   if ((rc = psso_create(cfg, &c)) != PSSO_OK) { c = nullptr; cleanup(); return rc; }
+  mark("create");
   if ((rc = psso_bind(c, &b, s)) || (rc = psso_init(c))) { cleanup(); return rc; }
   int64_t bt, bi;
   if ((rc = psso_check(c, &bt, &bi)) != PSSO_OK) {
@@ -1532,21 +1548,26 @@ int psso_solve(const psso_config* cfg, int64_t niter, double* traj, void* best_p
     cleanup();
     return rc;
   }
+  mark("init");
   cudaEventRecord(e0, s);
   if ((rc = psso_run(c, 0, niter)) != PSSO_OK) { cleanup(); return rc; }
   cudaEventRecord(e1, s);
+  mark("enqueue");
   if ((rc = psso_check(c, &bt, &bi)) != PSSO_OK) {
     g_err = "non-finite fitness at particle " + std::to_string(bi) + " at iteration " + std::to_string(bt);
     cleanup();
     return rc;
   }
+  mark("loop+sync");
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
   if (traj) e = cudaMemcpy(traj, b.traj, (size_t)niter * 8, cudaMemcpyDeviceToHost);
   if (e == cudaSuccess && best_position) e = cudaMemcpy(best_position, b.gbest, D * es, cudaMemcpyDeviceToHost);
   if (e == cudaSuccess && best_fitness) e = cudaMemcpy(best_fitness, b.g_f, 8, cudaMemcpyDeviceToHost);
   if (wall_s) *wall_s = ms * 1e-3;
+  mark("copy-back");
   cleanup();
+  mark("cleanup");
   if (e != cudaSuccess) return cuda_fail(nullptr, e, "psso_solve copy-back");
   return PSSO_OK;
 }
