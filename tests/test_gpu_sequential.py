@@ -201,3 +201,43 @@ def test_sequential_batch_c1_appendix_value():
                        niter=1000)
     recs = psso.run_sequential_batch(p, fn, [1, 0])
     assert recs[1].best_fitness == 10.383304882651581
+
+
+def test_sequential_nonfinite_on_a_cluster_names_first_particle():
+    """300 rows -> a 5-CTA cluster: the first serial-order probe hit, across CTA boundaries."""
+    level = float(O.init_positions(1, 300, 4, -1.0, 1.0)[:, 0].max())
+    fn = psso.probe_function(4, level=level, bounds=(-1.0, 1.0))
+    p = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=-1, var_max=1, nsol=300, nvar=4, niter=300)
+    with pytest.raises(psso.NonFiniteFitnessError) as ei:
+        psso.run_sequential(p, fn, seed=1)
+    err = ei.value
+    o = O.Oracle("f1", 300, 4, 0.3, 0.6, 0.8, -1.0, 1.0, 1)
+    sw = o.initialize()
+    for t in range(p.niter):
+        o.step_sequential(sw, t)
+        bad = np.nonzero(sw.sol[:, 0] > level)[0]
+        if bad.size:
+            assert (t, int(bad[0])) == (err.iteration, err.particle)
+            break
+    else:
+        pytest.fail("oracle replay never hit the probe")
+
+
+def test_sequential_batch_nonfinite_names_particle():
+    fn = psso.probe_function(8, level=0.999, bounds=(-1.0, 1.0))  # +inf once x[0] > 0.999
+    p = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=-1, var_max=1, nsol=64, nvar=8, niter=400)
+    with pytest.raises(psso.NonFiniteFitnessError) as ei:
+        psso.run_sequential_batch(p, fn, [0, 1, 2])
+    assert ei.value.particle >= 0 and ei.value.iteration is not None
+
+
+@pytest.mark.parametrize("g", ["1", "3", "16"])
+def test_sequential_cluster_size_does_not_change_results(g, monkeypatch):
+    fn = psso.make_function("f5", 40)
+    p = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=fn.var_min, var_max=fn.var_max,
+                       nsol=500, nvar=40, niter=25)
+    ref = psso.run_sequential(p, fn, 9)
+    monkeypatch.setenv("PSSO_SEQ_G", g)
+    rec = psso.run_sequential(p, fn, 9)
+    assert np.array_equal(rec.best_position, ref.best_position)
+    assert np.array_equal(rec.trajectory, ref.trajectory)
