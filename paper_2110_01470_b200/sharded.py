@@ -76,6 +76,10 @@ class ProcessGroupExchange:
         import torch.distributed as dist
 
         (c,) = cands
+        if c.is_cuda and dist.get_backend(self.group) != "nccl":  # gloo: stage through the host
+            out = c.new_empty(self.world * c.numel(), device="cpu")
+            dist.all_gather_into_tensor(out, c.cpu(), group=self.group)
+            return out.to(c.device)
         out = c.new_empty(self.world * c.numel())
         dist.all_gather_into_tensor(out, c, group=self.group)
         return out

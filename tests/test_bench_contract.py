@@ -5,6 +5,8 @@ import subprocess
 import sys
 from pathlib import Path
 
+import pytest
+
 ROOT = Path(__file__).resolve().parent.parent
 
 
@@ -34,3 +36,34 @@ def test_warmup_floor_enforced():
     out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--warmup", "2"],
                          capture_output=True, text=True, timeout=120, cwd=ROOT)
     assert out.returncode != 0 and "warmup" in out.stderr
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("exchange", ["collective", "p2p"])
+def test_bench_multi_rank_path_runs_under_torchrun(exchange):
+    """bench.py --gpus 2 under torchrun: the sharded path end to end.  Both ranks
+    share the one GPU of the box (gloo process group; runs use NCCL)."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ, PSSO_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"),
+           "--gpus", "2", "--steps", "6", "--warmup", "3", "--workload", "c3sphere",
+           "--exchange", exchange]
+    out = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(ln) for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["config"]["nsol"] == 2 * (1 << 20) and d["value"] > 0
+    assert d["gpu_launches"] > 0 and d["roofline"]["achieved"] > 0
