@@ -200,3 +200,35 @@ class DeviceEngine:
             self.p_f.copy_(torch.as_tensor(np.ascontiguousarray(swarm.p_f[lo:hi], dtype=np.float64)))
             self.g_f.fill_(float(swarm.g_f))
         self.stream.synchronize()
+
+    # -- checkpoint / resume ---------------------------------------
+    def save_state(self, path, t_next: int) -> None:
+        """Checkpoint the swarm before iteration ``t_next``.
+
+        The keyed RNG makes ``(X, P, p_f, gbest, g_f, t)`` the whole state of a
+        run (reference test_core.py:186-191: a shorter run is an exact prefix),
+        so a run restored from this file continues bit for bit.
+        """
+        sw = self.to_host()
+        np.savez(path, sol=sw.sol, pbests=sw.pbests, sol_f=sw.sol_f, p_f=sw.p_f, gbest=sw.gbest,
+                 g_f=np.float64(sw.g_f), t_next=np.int64(t_next), seed=np.uint64(self.seed & _MASK64),
+                 rows=np.int64([self.row_lo, self.row_hi]), dtype=np.str_(self.dtype),
+                 traj=self.traj.cpu().numpy())
+
+    def restore_state(self, path) -> int:
+        """Load a checkpoint written by :meth:`save_state`; returns the next iteration."""
+        import torch
+
+        z = np.load(path)
+        if (int(z["seed"]) != (self.seed & _MASK64) or str(z["dtype"]) != self.dtype
+                or list(z["rows"]) != [self.row_lo, self.row_hi]
+                or z["sol"].shape != tuple(self.sol.shape)):
+            raise ValueError("checkpoint does not match this engine (seed, dtype, rows or shape)")
+        self.load(Swarm(sol=z["sol"], pbests=z["pbests"], gbest=z["gbest"], sol_f=z["sol_f"],
+                        p_f=z["p_f"], g_f=float(z["g_f"])))
+        n = min(len(z["traj"]), self.traj.numel())
+        with torch.cuda.stream(self.stream):
+            self.traj[:n].copy_(torch.as_tensor(z["traj"][:n]))
+        self.stream.synchronize()
+        return int(z["t_next"])
+

@@ -241,3 +241,43 @@ def test_sequential_cluster_size_does_not_change_results(g, monkeypatch):
     rec = psso.run_sequential(p, fn, 9)
     assert np.array_equal(rec.best_position, ref.best_position)
     assert np.array_equal(rec.trajectory, ref.trajectory)
+
+
+@pytest.mark.parametrize("schedule", ["parallel", "sequential"])
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_checkpoint_resume_is_bitwise(schedule, dtype, tmp_path):
+    """save_state at t=25, restore into a fresh engine, run 20 more == 45 straight."""
+    fn = psso.make_function("f4", 64)
+    p = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=fn.var_min, var_max=fn.var_max,
+                       nsol=3000, nvar=64, niter=45)
+
+    def go(e, t0, n):
+        (e.run if schedule == "parallel" else e.run_sequential)(t0, n)
+
+    a = DeviceEngine(p, fn, 5, dtype=dtype)
+    a.initialize()
+    go(a, 0, 25)
+    a.save_state(tmp_path / "ck.npz", 25)
+    a.close()
+    b = DeviceEngine(p, fn, 5, dtype=dtype)
+    t = b.restore_state(tmp_path / "ck.npz")
+    go(b, t, 45 - t)
+    b.check()
+    c = DeviceEngine(p, fn, 5, dtype=dtype)
+    c.initialize()
+    go(c, 0, 45)
+    try:
+        sb, sc = b.to_host(), c.to_host()
+        assert t == 25
+        assert np.array_equal(sb.sol, sc.sol) and np.array_equal(sb.pbests, sc.pbests)
+        assert np.array_equal(sb.gbest, sc.gbest) and sb.g_f == sc.g_f
+        assert np.array_equal(b.traj.cpu().numpy(), c.traj.cpu().numpy())
+    finally:
+        b.close()
+        c.close()
+    other = DeviceEngine(p, fn, 6, dtype=dtype)
+    try:
+        with pytest.raises(ValueError, match="does not match"):
+            other.restore_state(tmp_path / "ck.npz")
+    finally:
+        other.close()
