@@ -159,12 +159,33 @@ def test_sequential_nonfinite_names_first_particle():
         pytest.fail("oracle replay never hit the probe")
 
 
-def test_sequential_rejects_unsupported_shapes():
+def test_sequential_kernel_rejects_long_rows():
+    """psso_run_sequential (k_seq) takes nvar <= 128; run_sequential covers the rest host-driven."""
     fn = psso.make_function("f1", 200)
     p = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=-5.12, var_max=5.12, nsol=10, nvar=200,
                        niter=3)
-    with pytest.raises(psso._lib.PssoError, match="nvar <= 128"):
-        psso.run_sequential(p, fn, seed=0)
+    eng = DeviceEngine(p, fn, 0)
+    try:
+        eng.initialize()
+        with pytest.raises(psso._lib.PssoError, match="nvar <= 128"):
+            eng.run_sequential(0, 3)
+    finally:
+        eng.close()
+
+
+@pytest.mark.parametrize("fid,nsol,nvar,niter", [("f1", 60, 200, 12), ("f5", 40, 300, 10),
+                                                  ("f4", 30, 512, 8), ("f7", 25, 129, 10)])
+def test_sequential_long_rows_against_oracle(fid, nsol, nvar, niter):
+    fn = _fn(fid, nvar)
+    p = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=fn.var_min, var_max=fn.var_max,
+                       nsol=nsol, nvar=nvar, niter=niter)
+    rec = psso.run_sequential(p, fn, 31)
+    o = O.Oracle.from_params(p, fid, 31)
+    osw = o.initialize()
+    otraj = o.run_sequential(osw, 0, niter)
+    assert rec.schedule == psso.ScheduleKind.SEQUENTIAL
+    assert np.array_equal(rec.best_position, osw.gbest)
+    assert _close(rec.trajectory, otraj, fid)
 
 
 def test_sequential_fp32_and_philox_modes_run():
