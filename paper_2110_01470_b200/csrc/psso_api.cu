@@ -1154,8 +1154,7 @@ int psso_run(psso_ctx* c, int64_t t0, int64_t niter) {
 // row group per warp, which beats fewer CTAs with more groups per warp even
 // at C1 (100 rows: G = 2 6.2 ms, G = 1 9.6 ms per 1000 iterations);
 // PSSO_SEQ_G overrides.  Rows are split in blocks of rpc.
-static cudaError_t launch_seq(psso_ctx* c, const void* f, int M, SeqParams q, int64_t B,
-                              cudaStream_t s) {
+static cudaError_t launch_seq(psso_ctx* c, int M, SeqParams q, int64_t B, cudaStream_t s) {
   const psso_config* cfg = &c->cfg;
   const int es = cfg->dtype == PSSO_F64 ? 8 : 4;
   const int nw = PSSO_SEQ_NT / 32;
@@ -1170,7 +1169,16 @@ static cudaError_t launch_seq(psso_ctx* c, const void* f, int M, SeqParams q, in
   p.off_bar = (int)align16((size_t)p.off_red + 16 * nw + 64 * M);
   p.off_scr = (int)align16((size_t)p.off_bar + 8 * (nw + 2));
   p.off_leaf = (int)align16((size_t)p.off_scr + (smem_fn ? (size_t)nw * 4 * (8 * M) * es : 0));
-  const size_t smem = (size_t)p.off_leaf + 32 + 2 * (size_t)cfg->nvar * es;
+  size_t smem = (size_t)p.off_leaf + 32 + 2 * (size_t)cfg->nvar * es;
+  // RES: the CTA's rows (X, P, speculative rows, p_f, fitness) resident in
+  // shared memory when they fit (C2 shape: 64 rows x 100), else global memory
+  p.off_xs = (int)align16(smem);
+  const size_t smem_res = (size_t)p.off_xs + 3 * (size_t)q.rpc * cfg->nvar * es + 16 * (size_t)q.rpc;
+  const char* nr = std::getenv("PSSO_SEQ_NO_RES");
+  const bool res = smem_res <= 227 * 1024 && !(nr && *nr && *nr != '0');
+  if (res) smem = smem_res;
+  const void* f = seq_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, M, res);
+  if (!f) return cudaErrorInvalidDeviceFunction;
   cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess && G > 8) e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return e;
@@ -1205,8 +1213,8 @@ int psso_run_sequential(psso_ctx* c, int64_t t0, int64_t niter) {
   const int64_t rows = cfg->nsol, D = cfg->nvar;
   const int M = D <= 32 ? 4 : D <= 64 ? 8 : 16;
   const int es = cfg->dtype == PSSO_F64 ? 8 : 4;
-  const void* f = seq_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, M);
-  if (!f) return fail(c, PSSO_E_UNSUPPORTED, "no sequential kernel for this configuration");
+  if (!seq_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, M, false))
+    return fail(c, PSSO_E_UNSUPPORTED, "no sequential kernel for this configuration");
   if (!c->seq_xn) {
     const uint64_t seed = cfg->seed;
     CK(c, cudaMalloc(&c->seq_xn, (size_t)rows * D * es));
@@ -1234,7 +1242,7 @@ int psso_run_sequential(psso_ctx* c, int64_t t0, int64_t niter) {
   q.sol_f = c->buf.sol_f;
   q.bad = c->bad;
   q.passes = c->seq_passes;
-  CK(c, launch_seq(c, f, M, q, 1, c->stream));
+  CK(c, launch_seq(c, M, q, 1, c->stream));
   return PSSO_OK;
 }
 
@@ -1674,8 +1682,10 @@ static int solve_batch(const psso_config* cfg, const uint64_t* seeds, int32_t ns
   sp.niter = niter;
   if (sequential) {  // speculative-pass scratch of k_seq, then its loop
     const int M = D <= 32 ? 4 : D <= 64 ? 8 : 16;
-    const void* f = seq_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, M);
-    if (!f) { cleanup(); return fail(nullptr, PSSO_E_UNSUPPORTED, "no sequential kernel for this configuration"); }
+    if (!seq_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, M, false)) {
+      cleanup();
+      return fail(nullptr, PSSO_E_UNSUPPORTED, "no sequential kernel for this configuration");
+    }
     if ((e = pool_alloc(&xn.p, B * N * D * es, s)) != cudaSuccess ||
         (e = pool_alloc(&fn.p, B * N * 8, s)) != cudaSuccess ||
         (e = pool_alloc(&pfn.p, B * N * 8, s)) != cudaSuccess) {
@@ -1697,7 +1707,7 @@ static int solve_batch(const psso_config* cfg, const uint64_t* seeds, int32_t ns
     q.seeds = (const uint64_t*)sd.p;
     q.bad = (unsigned long long*)bad.p;
     cudaEventRecord(e0, s);
-    if ((e = launch_seq(c, f, M, q, (int64_t)B, s)) != cudaSuccess) {
+    if ((e = launch_seq(c, M, q, (int64_t)B, s)) != cudaSuccess) {
       cleanup();
       return cuda_fail(nullptr, e, "psso_solve_sequential_batch run");
     }

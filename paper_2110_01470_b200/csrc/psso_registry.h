@@ -33,14 +33,14 @@ inline const void* swarm_kernel(int dtype, int rng, int fn, int m, bool res, boo
   return rng == 0 ? swarm_kernel_f32_ref(fn, m, res, cl) : swarm_kernel_f32_philox(fn, m, res, cl);
 }
 
-const void* seq_kernel_f64_ref(int fn, int m);
-const void* seq_kernel_f64_philox(int fn, int m);
-const void* seq_kernel_f32_ref(int fn, int m);
-const void* seq_kernel_f32_philox(int fn, int m);
+const void* seq_kernel_f64_ref(int fn, int m, bool res);
+const void* seq_kernel_f64_philox(int fn, int m, bool res);
+const void* seq_kernel_f32_ref(int fn, int m, bool res);
+const void* seq_kernel_f32_philox(int fn, int m, bool res);
 
-inline const void* seq_kernel(int dtype, int rng, int fn, int m) {
-  if (dtype == 0) return rng == 0 ? seq_kernel_f64_ref(fn, m) : seq_kernel_f64_philox(fn, m);
-  return rng == 0 ? seq_kernel_f32_ref(fn, m) : seq_kernel_f32_philox(fn, m);
+inline const void* seq_kernel(int dtype, int rng, int fn, int m, bool res) {
+  if (dtype == 0) return rng == 0 ? seq_kernel_f64_ref(fn, m, res) : seq_kernel_f64_philox(fn, m, res);
+  return rng == 0 ? seq_kernel_f32_ref(fn, m, res) : seq_kernel_f32_philox(fn, m, res);
 }
 
 inline const void* chain_kernel(int dtype, int rng, int fn, int m, bool init, bool full) {

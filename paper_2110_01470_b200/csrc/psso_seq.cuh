@@ -62,7 +62,8 @@ struct SeqParams {
 //   off_bar  first-event reduction: NW int64 + 2
 //   off_scr  per-warp smem rows [4][8M] (f3, f7, f8)
 //   off_leaf published event records [2][row index, fitness] + rows [2][D]
-template <typename T, int FN, int RNG, int M>
+//   off_xs   RES: this CTA's rows resident for the launch: X, P, Xn [rpc][D], p_f, fn [rpc]
+template <typename T, int FN, int RNG, int M, bool RES>
 __global__ void __launch_bounds__(PSSO_SEQ_NT, 1)
     k_seq(const __grid_constant__ TileParams p, const __grid_constant__ SeqParams q) {
   constexpr int NTC = PSSO_SEQ_NT;
@@ -85,11 +86,19 @@ __global__ void __launch_bounds__(PSSO_SEQ_NT, 1)
   namespace cgx = cooperative_groups;
   cgx::cluster_group cluster = cgx::this_cluster();
 
-  T* X = reinterpret_cast<T*>(p.X) + (int64_t)b * rows * D;
-  T* P = reinterpret_cast<T*>(p.P) + (int64_t)b * rows * D;
-  double* pf = p.p_f + (int64_t)b * rows;
-  T* Xn = reinterpret_cast<T*>(q.Xn) + (int64_t)b * rows * D;
-  double* fn = q.fn + (int64_t)b * rows;
+  T* Xg = reinterpret_cast<T*>(p.X) + (int64_t)b * rows * D;
+  T* Pg = reinterpret_cast<T*>(p.P) + (int64_t)b * rows * D;
+  double* pfg = p.p_f + (int64_t)b * rows;
+  // RES: the CTA's rows live in shared memory for the whole launch (indexed
+  // from base = r0); else everything stays in global memory (base = 0)
+  const int64_t base = RES ? r0 : 0;
+  const int64_t nres = RES ? (int64_t)q.rpc : 0;
+  T* Xs = reinterpret_cast<T*>(smem + p.off_xs);
+  T* X = RES ? Xs : Xg;
+  T* P = RES ? Xs + nres * D : Pg;
+  T* Xn = RES ? Xs + 2 * nres * D : reinterpret_cast<T*>(q.Xn) + (int64_t)b * rows * D;
+  double* pf = RES ? reinterpret_cast<double*>(Xs + 3 * nres * D) : pfg;
+  double* fn = RES ? pf + nres : q.fn + (int64_t)b * rows;
   double* sf = q.sol_f ? q.sol_f + (int64_t)b * rows : nullptr;
   T* gbp = reinterpret_cast<T*>(q.gbest) + (int64_t)b * D;
   unsigned long long* bad = q.bad + b;
@@ -102,10 +111,10 @@ __global__ void __launch_bounds__(PSSO_SEQ_NT, 1)
   ev.aux = stage_aux<FN>(p.aux, p.D);
   ev.X = Xn;
   ev.P = Xn;
-  ev.p_f = q.pfn + (int64_t)b * rows;
+  ev.p_f = q.pfn + (int64_t)b * rows + base;
   ev.sol_f = fn;
   ev.bad = nullptr;
-  ev.row_lo = 0;
+  ev.row_lo = base;
   ev.seed = q.seeds[b];
   ev.D = D;
   ev.n = p.plan.n;
@@ -116,6 +125,13 @@ __global__ void __launch_bounds__(PSSO_SEQ_NT, 1)
   for (int q8 = tid; q8 < 8 * M; q8 += NTC) {
     xg[q8] = xs30(GAMMA * (uint64_t)(q8 + 1));
     gb[q8] = q8 < D ? gbp[q8] : (T)0;
+  }
+  if constexpr (RES) {  // this CTA's rows -> shared memory
+    for (int64_t e = tid; e < (r1 - r0) * D; e += NTC) {
+      X[e] = Xg[r0 * D + e];
+      P[e] = Pg[r0 * D + e];
+    }
+    for (int64_t r = tid; r < r1 - r0; r += NTC) pf[r] = pfg[r0 + r];
   }
   double gf = q.g_f[b];
   int64_t npass = 0;
@@ -142,9 +158,9 @@ __global__ void __launch_bounds__(PSSO_SEQ_NT, 1)
         const int64_t r = 4 * grp + (lane >> 3);
         const bool rv = r < r1 && r >= a0;
         const int64_t rl = r < r1 ? r : r1 - 1;
-        const double pf_row = pf[rl];
-        const T* xl = X + rl * (int64_t)D;
-        const T* pl = P + rl * (int64_t)D;
+        const double pf_row = pf[rl - base];
+        const T* xl = X + (rl - base) * (int64_t)D;
+        const T* pl = P + (rl - base) * (int64_t)D;
         T x[M], pv[M];
 #pragma unroll
         for (int m = 0; m < M; ++m) {
@@ -152,15 +168,15 @@ __global__ void __launch_bounds__(PSSO_SEQ_NT, 1)
           x[m] = j < D ? xl[j] : (T)0;
           pv[m] = j < D ? pl[j] : (T)0;
         }
-        chain_step<T, FN, RNG, M, false, false, true>(p, ev, gb, xg, scr, r, rv, x, pv, pf_row,
+        chain_step<T, FN, RNG, M, false, false, true>(p, ev, gb, xg, scr, r - base, rv, x, pv, pf_row,
                                                       best_f, best_i, best_new);
       }
       __syncthreads();  // Xn / fn of the pass visible to the CTA
       // ---- this CTA's first event: non-finite (core.py:233) or a gbest move (core.py:236-241)
       int64_t ev_r = INT64_MAX;
       for (int64_t r = a0 + tid; r < r1; r += NTC) {
-        const double f = fn[r];
-        if (!isfinite(f) || (f <= pf[r] && f <= gf)) { ev_r = r; break; }
+        const double f = fn[r - base];
+        if (!isfinite(f) || (f <= pf[r - base] && f <= gf)) { ev_r = r; break; }
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) ev_r = min(ev_r, __shfl_xor_sync(0xffffffffu, ev_r, o));
@@ -172,7 +188,7 @@ __global__ void __launch_bounds__(PSSO_SEQ_NT, 1)
         for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
         if (lane == 0) {
           pub_i[par] = v;
-          pub_f[par] = v != INT64_MAX ? fn[v] : 0.0;
+          pub_f[par] = v != INT64_MAX ? fn[v - base] : 0.0;
           red[NW] = v;
         }
       }
@@ -180,7 +196,7 @@ __global__ void __launch_bounds__(PSSO_SEQ_NT, 1)
       {  // publish the event row (read by every CTA after the barrier)
         const int64_t v = red[NW];
         if (v != INT64_MAX)
-          for (int j = tid; j < D; j += NTC) pub_row[par * D + j] = Xn[v * (int64_t)D + j];
+          for (int j = tid; j < D; j += NTC) pub_row[par * D + j] = Xn[(v - base) * (int64_t)D + j];
       }
       cluster.sync();  // every CTA's record of this pass is published
       if (warp == 0) {  // lowest-index event over the cluster (DSMEM)
@@ -204,20 +220,20 @@ __global__ void __launch_bounds__(PSSO_SEQ_NT, 1)
       const int64_t hi = min(rs, r1 - 1);  // last committed row of this CTA
       // ---- commit this CTA's rows a0..hi: X always (core.py:231), pBest on `<=` (:236-238)
       for (int64_t r = a0 + warp; r <= hi; r += NW) {
-        const double f = fn[r];
-        const bool imp = isfinite(f) && f <= pf[r];
-        const T* src = Xn + r * (int64_t)D;
+        const double f = fn[r - base];
+        const bool imp = isfinite(f) && f <= pf[r - base];
+        const T* src = Xn + (r - base) * (int64_t)D;
         for (int j = lane; j < D; j += 32) {
           const T v = src[j];
-          X[r * (int64_t)D + j] = v;
-          if (imp) P[r * (int64_t)D + j] = v;
+          X[(r - base) * (int64_t)D + j] = v;
+          if (imp) P[(r - base) * (int64_t)D + j] = v;
         }
       }
       __syncthreads();  // pBest rows copied before p_f moves
       for (int64_t r = a0 + tid; r <= hi; r += NTC) {
-        const double f = fn[r];
+        const double f = fn[r - base];
         if (sf) sf[r] = f;
-        if (isfinite(f) && f <= pf[r]) pf[r] = f;
+        if (isfinite(f) && f <= pf[r - base]) pf[r - base] = f;
       }
       if (rs != INT64_MAX) {
         const double f = cluster.map_shared_rank(pub_f, own)[par];
@@ -236,6 +252,14 @@ __global__ void __launch_bounds__(PSSO_SEQ_NT, 1)
       lo = rs != INT64_MAX ? rs + 1 : rows;
     }
     if (!stop && c == 0 && tid == 0 && q.traj) q.traj[b * q.traj_stride + t] = gf;  // core.py:242
+  }
+  if constexpr (RES) {  // the CTA's rows back to global memory
+    __syncthreads();
+    for (int64_t e = tid; e < (r1 - r0) * D; e += NTC) {
+      Xg[r0 * D + e] = X[e];
+      Pg[r0 * D + e] = P[e];
+    }
+    for (int64_t r = tid; r < r1 - r0; r += NTC) pfg[r0 + r] = pf[r];
   }
   if (c == 0) {
     for (int j = tid; j < D; j += NTC) gbp[j] = gb[j];

@@ -26,14 +26,14 @@ const void* PSSO_NAME(swarm_kernel)(int fn, int m, bool res, bool cl) {
   }
 }
 
-#define PSSO_SEQ(FN)                                                    \
-  case FN:                                                              \
-    if (m == 4) return (const void*)k_seq<PSSO_T, FN, PSSO_RNG, 4>;     \
-    if (m == 8) return (const void*)k_seq<PSSO_T, FN, PSSO_RNG, 8>;     \
-    if (m == 16) return (const void*)k_seq<PSSO_T, FN, PSSO_RNG, 16>;   \
-    return nullptr;
+#define PSSO_SEQ_M(FN, M)                                                          \
+  if (m == M) return res ? (const void*)k_seq<PSSO_T, FN, PSSO_RNG, M, true>        \
+                         : (const void*)k_seq<PSSO_T, FN, PSSO_RNG, M, false>;
+#define PSSO_SEQ(FN) \
+  case FN:           \
+    PSSO_SEQ_M(FN, 4) PSSO_SEQ_M(FN, 8) PSSO_SEQ_M(FN, 16) return nullptr;
 
-const void* PSSO_NAME(seq_kernel)(int fn, int m) {
+const void* PSSO_NAME(seq_kernel)(int fn, int m, bool res) {
   switch (fn) {
     PSSO_SEQ(0) PSSO_SEQ(1) PSSO_SEQ(2) PSSO_SEQ(3) PSSO_SEQ(4)
     PSSO_SEQ(5) PSSO_SEQ(6) PSSO_SEQ(7) PSSO_SEQ(8) PSSO_SEQ(9)

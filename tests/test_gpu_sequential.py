@@ -302,3 +302,25 @@ def test_checkpoint_resume_is_bitwise(schedule, dtype, tmp_path):
             other.restore_state(tmp_path / "ck.npz")
     finally:
         other.close()
+
+
+@pytest.mark.parametrize("fid,nsol,nvar", [("f5", 1024, 100), ("f7", 300, 77), ("f3", 200, 64)])
+def test_sequential_resident_rows_equal_global_rows(fid, nsol, nvar, monkeypatch):
+    """k_seq with the CTA's rows in shared memory == rows in global memory, bit for bit."""
+    fn = _fn(fid, nvar)
+    p = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=fn.var_min, var_max=fn.var_max,
+                       nsol=nsol, nvar=nvar, niter=30)
+    outs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("PSSO_SEQ_NO_RES", flag)
+        eng = DeviceEngine(p, fn, 12)
+        try:
+            eng.initialize()
+            eng.run_sequential(0, 30)
+            eng.check()
+            outs.append((eng.to_host(), eng.traj.cpu().numpy()))
+        finally:
+            eng.close()
+    (a, ta), (b, tb) = outs
+    assert np.array_equal(a.sol, b.sol) and np.array_equal(a.pbests, b.pbests)
+    assert np.array_equal(a.p_f, b.p_f) and np.array_equal(ta, tb)
