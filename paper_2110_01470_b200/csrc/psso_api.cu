@@ -655,6 +655,10 @@ bool plan_swarm(psso_ctx* c, int64_t B, SwarmPlan& sp, cudaError_t& e) {
     const char* gs = std::getenv("PSSO_SWARM_G");
     // about half the warps of each CTA busy: shorter per-CTA chains beat fewer CTAs
     int64_t G = std::max<int64_t>(1, std::min<int64_t>(16, (ngroups + 7) / 8));
+    // a batch: no more clusters than fit one wave (B * G <= SMs) while the
+    // CTA's rows still fit in shared memory -- a second wave doubles the time
+    if (B > 1)
+      while (G > 1 && B * G > c->num_sms && res_smem((ngroups + G - 2) / (G - 1)) <= 227 * 1024) --G;
     if (gs && *gs) G = std::max<int64_t>(1, std::min<int64_t>(16, std::atoll(gs)));
     const int64_t gpc = (ngroups + G - 1) / G;
     G = (ngroups + gpc - 1) / gpc;
