@@ -193,11 +193,19 @@ __global__ void __launch_bounds__(PSSO_SWARM_NT, 1)
     }
     if (lane == 0) { red_f[warp] = best_f; red_i[warp] = best_i; red_n[warp] = best_new; }
     __syncthreads();
+    if (warp == 0) {  // the CTA's NW warp candidates, reduced by warp 0 with shuffles
+      best_f = lane < NW ? red_f[lane] : CUDART_INF;
+      best_i = lane < NW ? red_i[lane] : INT64_MAX;
+      best_new = lane < NW ? red_n[lane] : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double of = __shfl_xor_sync(0xffffffffu, best_f, o);
+        const int64_t oi = __shfl_xor_sync(0xffffffffu, best_i, o);
+        const int on = __shfl_xor_sync(0xffffffffu, best_new, o);
+        if (lex_less(of, oi, best_f, best_i)) { best_f = of; best_i = oi; best_new = on; }
+      }
+    }
     if (tid == 0) {
-      for (int w = 1; w < NW; ++w)
-        if (lex_less(red_f[w], red_i[w], best_f, best_i)) {
-          best_f = red_f[w]; best_i = red_i[w]; best_new = red_n[w];
-        }
       const int seen_bad = *(volatile unsigned long long*)ev.bad != ~0ull;
       if constexpr (CL) {
         pub_f[par] = best_f;
