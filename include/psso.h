@@ -142,7 +142,11 @@ int psso_update_gbest(psso_ctx* ctx);
 
 /* Sharded (multi-rank) iteration, split around the gBest exchange.
  * A candidate record is psso_candidate_bytes(cfg) bytes:
- *   float64 p_f, int64 global index, then nvar elements of dtype (the row).
+ *   float64 p_f, int64 global index, uint64 the shard's first non-finite key
+ *   ((t+1) << 40 | i, all ones if none), float64 that fitness value, then nvar
+ *   elements of dtype (the row) at offset 32.  Applying the records also
+ *   adopts the smallest non-finite key, so every shard stops at the same
+ *   iteration and psso_check reports the same first (t, i) on every rank.
  * psso_step_local: fused kernel over this context's rows, then the local
  * stage-2 reduction, writing this rank's record to `cand` (device).
  * psso_apply_candidates: lexicographic (p_f, index) min over `ncand` gathered
@@ -183,6 +187,23 @@ int psso_apply_p2p(psso_ctx* ctx, int64_t t, const void* my_buf, int32_t nranks,
  * far as (iteration, particle); iteration -1 = initialization.  Returns
  * PSSO_E_NONFINITE if there was one (core.py:190-193 semantics). */
 int psso_check(psso_ctx* ctx, int64_t* bad_t, int64_t* bad_i);
+
+/* replaces: reading Swarm.g_f and the gBest argmin index after a run
+ * (parallel.py:208-211 select `best = min(candidates)`; core.py:202 at
+ * initialization).  Synchronizes the stream; writes the gBest fitness and the
+ * GLOBAL particle index whose pBest row is gbest (-1 before psso_init), and
+ * the first non-finite fitness like psso_check.  Any output may be NULL.
+ * Returns PSSO_E_NONFINITE (outputs still written) if there was one. */
+int psso_result(psso_ctx* ctx, double* g_f, int64_t* g_idx, int64_t* bad_t, int64_t* bad_i);
+
+/* psso_check plus the non-finite fitness value (NonFiniteFitnessError.value,
+ * core.py:43-53), also on shards that do not own the failing particle (the
+ * value travels in the candidate records).  *value = 0 when there is none. */
+int psso_nonfinite(psso_ctx* ctx, int64_t* bad_t, int64_t* bad_i, double* value);
+
+/* Sets the gBest index psso_result reports, for swarm state uploaded by the
+ * host (a checkpoint, a Swarm handed to the phase API).  Asynchronous. */
+int psso_set_gbest_index(psso_ctx* ctx, int64_t g_idx);
 
 /* Number of kernels this context has launched (for launch accounting). */
 int64_t psso_launch_count(const psso_ctx* ctx);

@@ -30,7 +30,8 @@ EXPORTS = (
     "psso_version", "psso_last_error", "psso_create", "psso_destroy", "psso_bind",
     "psso_init", "psso_step", "psso_run", "psso_search", "psso_evaluate",
     "psso_update_pbests", "psso_update_gbest", "psso_candidate_bytes", "psso_init_local",
-    "psso_step_local", "psso_apply_candidates", "psso_check", "psso_launch_count",
+    "psso_step_local", "psso_apply_candidates", "psso_check", "psso_result", "psso_set_gbest_index", "psso_nonfinite",
+    "psso_launch_count",
     "psso_rng_uniform", "psso_eval_rows", "psso_solve", "psso_profile", "psso_profile_read",
     "psso_kernel_name", "psso_solve_batch", "psso_p2p_buffer_bytes", "psso_p2p_alloc",
     "psso_p2p_free", "psso_p2p_handle", "psso_p2p_open", "psso_p2p_close", "psso_publish_p2p",
@@ -113,6 +114,10 @@ def load():
     L.psso_step_local.argtypes = [vp, i64, vp]
     L.psso_apply_candidates.argtypes = [vp, i64, vp, i32, i32]
     L.psso_check.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.psso_set_gbest_index.argtypes = [vp, i64]
+    L.psso_nonfinite.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(dbl)]
+    L.psso_result.argtypes = [vp, ctypes.POINTER(dbl), ctypes.POINTER(i64), ctypes.POINTER(i64),
+                              ctypes.POINTER(i64)]
     L.psso_launch_count.argtypes = [vp]
     L.psso_launch_count.restype = i64
     L.psso_profile.argtypes = [vp, i32]

@@ -178,7 +178,17 @@ struct GbParams {
   int64_t* t_dev;        // if non-null: t read here and incremented
   int32_t is_init;
   int32_t pad;
+  int64_t* g_idx;        // gBest particle index (parallel.py:208-211), may be null
+  unsigned long long* bad;  // this shard's first non-finite key ((t+1) << 40 | i)
+  const double* sol_f;      // this shard's sol_f (the non-finite value), may be null
+  double* bad_val;          // value of the run's first non-finite fitness (sharded runs)
 };
+
+// Candidate record of a shard (psso_candidate_bytes): the exchange payload of
+// parallel.py:199-208 plus the shard's non-finite state, so that every shard
+// stops at the same iteration and reports the same first (t, i)
+// (core.py:190-193 over the whole swarm, not per shard).
+constexpr int64_t REC_HDR = 32;  // f64 p_f | i64 index | u64 non-finite key | f64 its value | row
 
 template <typename T>
 __device__ void block_argmin(const double* f, const int64_t* idx, int n, double& bf, int64_t& bi,
@@ -224,6 +234,7 @@ __global__ void __launch_bounds__(GB_THREADS) k_gbest(const __grid_constant__ Gb
   if (threadIdx.x == 0) {
     const double gf = take ? bf : inc;
     if (take) *g.g_f = gf;
+    if (take && g.g_idx) *g.g_idx = bi;
     const int64_t t = g.t_dev ? *g.t_dev : g.t_arg;
     if (g.traj && t >= 0) g.traj[t] = gf;
     if (g.t_dev) *g.t_dev = t + 1;
@@ -241,12 +252,43 @@ __global__ void __launch_bounds__(GB_THREADS) k_local_cand(const __grid_constant
   block_argmin<T>(g.slot_f, g.slot_i, g.nslots, bf, bi, sf, si);
   if (bi != INT64_MAX) {
     const T* src = reinterpret_cast<const T*>(g.P) + (bi - g.row_lo) * (int64_t)g.D;
-    T* dst = reinterpret_cast<T*>(rec + 16);
+    T* dst = reinterpret_cast<T*>(rec + REC_HDR);
     for (int j = threadIdx.x; j < g.D; j += blockDim.x) dst[j] = src[j];
   }
   if (threadIdx.x == 0) {
     *reinterpret_cast<double*>(rec) = bf;
     *reinterpret_cast<int64_t*>(rec + 8) = bi;
+    const unsigned long long key = g.bad ? *g.bad : ~0ull;
+    double v = 0.0;
+    if (key != ~0ull) {
+      const int64_t i = (int64_t)(key & ((1ull << 40) - 1));
+      if (g.sol_f && i >= g.row_lo) v = g.sol_f[i - g.row_lo];  // the owner's value
+      else if (g.bad_val) v = *g.bad_val;                       // learnt from an exchange
+    }
+    *reinterpret_cast<unsigned long long*>(rec + 16) = key;
+    *reinterpret_cast<double*>(rec + 24) = v;
+  }
+}
+
+// the run's first non-finite fitness over the gathered records: the minimum
+// key, adopted by this shard (so its later iterations are no-ops, like the
+// owner's) together with its value
+__device__ __forceinline__ void adopt_nonfinite(const GbParams& g, const unsigned char* recs,
+                                                int64_t rec_bytes, int n, bool cg) {
+  unsigned long long kmin = ~0ull;
+  double v = 0.0;
+  for (int k = 0; k < n; ++k) {
+    const unsigned char* r = recs + k * rec_bytes;
+    const unsigned long long key = cg ? (unsigned long long)__ldcg(reinterpret_cast<const long long*>(r + 16))
+                                      : *reinterpret_cast<const unsigned long long*>(r + 16);
+    if (key < kmin) {
+      kmin = key;
+      v = cg ? __ldcg(reinterpret_cast<const double*>(r + 24)) : *reinterpret_cast<const double*>(r + 24);
+    }
+  }
+  if (kmin != ~0ull && g.bad && kmin <= *g.bad) {
+    *g.bad = kmin;
+    if (g.bad_val) *g.bad_val = v;
   }
 }
 
@@ -267,18 +309,20 @@ __global__ void __launch_bounds__(GB_THREADS) k_apply(const __grid_constant__ Gb
       int64_t i = *reinterpret_cast<const int64_t*>(r + 8);
       if (lex_less(f, i, bf, bi)) { bf = f; bi = i; w = k; }
     }
+    adopt_nonfinite(g, recs, rec_bytes, ncand, false);
     const double inc = *g.g_f;
     take_s = bi != INT64_MAX && (g.is_init || bf <= inc);
     winner = w;
     const double gf = take_s ? bf : inc;
     if (take_s) *g.g_f = gf;
+    if (take_s && g.g_idx) *g.g_idx = bi;
     const int64_t t = g.t_dev ? *g.t_dev : g.t_arg;
     if (g.traj && t >= 0) g.traj[t] = gf;
     if (g.t_dev) *g.t_dev = t + 1;
   }
   __syncthreads();
   if (take_s) {
-    const T* src = reinterpret_cast<const T*>(recs + winner * rec_bytes + 16);
+    const T* src = reinterpret_cast<const T*>(recs + winner * rec_bytes + REC_HDR);
     T* dst = reinterpret_cast<T*>(g.gbest);
     for (int j = threadIdx.x; j < g.D; j += blockDim.x) dst[j] = src[j];
   }
@@ -345,17 +389,19 @@ __global__ void __launch_bounds__(GB_THREADS) k_apply_p2p(const __grid_constant_
       const int64_t i = __ldcg(reinterpret_cast<const long long*>(r + 8));
       if (lex_less(f, i, bf, bi)) { bf = f; bi = i; w = k; }
     }
+    adopt_nonfinite(g, recs, rec_bytes, R, true);
     const double inc = *g.g_f;
     take_s = bi != INT64_MAX && (g.is_init || bf <= inc);  // parallel.py:209
     winner = w;
     const double gf = take_s ? bf : inc;
     if (take_s) *g.g_f = gf;
+    if (take_s && g.g_idx) *g.g_idx = bi;
     if (g.traj && g.t_arg >= 0) g.traj[g.t_arg] = gf;
     __threadfence_block();
   }
   __syncthreads();
   if (take_s) {
-    const T* src = reinterpret_cast<const T*>(recs + winner * rec_bytes + 16);
+    const T* src = reinterpret_cast<const T*>(recs + winner * rec_bytes + REC_HDR);
     T* dst = reinterpret_cast<T*>(g.gbest);
     for (int j = threadIdx.x; j < g.D; j += blockDim.x) dst[j] = __ldcg(src + j);
   }
@@ -441,6 +487,8 @@ struct psso_ctx {
   int64_t* slot_i;
   unsigned long long* bad;
   int64_t* t_dev;
+  int64_t* g_idx;        // gBest particle index, -1 before initialization
+  double* bad_val;       // first non-finite value learnt from a candidate exchange
   double* aux;
   uint64_t Kw, Kp, Kg, Kw32, Kp32, Kg32;
   int64_t launches;
@@ -577,6 +625,10 @@ GbParams gb_params(psso_ctx* c, int64_t t, int64_t* t_dev, int is_init, int nslo
   g.t_arg = t;
   g.t_dev = t_dev;
   g.is_init = is_init;
+  g.g_idx = c->g_idx;
+  g.bad = c->bad;
+  g.sol_f = c->buf.sol_f;
+  g.bad_val = c->bad_val;
   return g;
 }
 
@@ -587,6 +639,19 @@ int launch_gbest(psso_ctx* c, const GbParams& g) {
   c->launches++;
   return PSSO_OK;
 }
+
+// Every context entry point runs on the context's device (the one current at
+// psso_create), whatever device the calling thread has current; the caller's
+// device is restored on return.
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(const psso_ctx* c) {
+    if (c && cudaGetDevice(&prev) == cudaSuccess && prev != c->device) cudaSetDevice(c->device);
+    else prev = -1;
+  }
+  ~DevGuard() { if (prev >= 0) cudaSetDevice(prev); }
+};
+#define DEV_GUARD(c) DevGuard dev_guard_(c)
 
 int need_bound(psso_ctx* c) {
   if (!c) return fail(nullptr, PSSO_E_INVALID, "null context");
@@ -949,6 +1014,9 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
       (e = cudaMalloc(&c->slot_i, sizeof(int64_t) * c->nslots)) != cudaSuccess ||
       (e = cudaMalloc(&c->bad, sizeof(unsigned long long))) != cudaSuccess ||
       (e = cudaMalloc(&c->t_dev, sizeof(int64_t))) != cudaSuccess ||
+      (e = cudaMalloc(&c->g_idx, sizeof(int64_t))) != cudaSuccess ||
+      (e = cudaMalloc(&c->bad_val, sizeof(double))) != cudaSuccess ||
+      (e = cudaMemset(c->g_idx, 0xff, sizeof(int64_t))) != cudaSuccess ||
       (e = cudaMemset(c->bad, 0xff, sizeof(unsigned long long))) != cudaSuccess) {
     psso_destroy(c);
     return cuda_fail(nullptr, e, "psso_create alloc");
@@ -985,12 +1053,15 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
 
 void psso_destroy(psso_ctx* c) {
   if (!c) return;
+  DEV_GUARD(c);
   if (c->graph) cudaGraphExecDestroy(c->graph);
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   cudaFree(c->slot_f);
   cudaFree(c->slot_i);
   cudaFree(c->bad);
   cudaFree(c->t_dev);
+  cudaFree(c->g_idx);
+  cudaFree(c->bad_val);
   cudaFree(c->aux);
   cudaFree(c->sw_epoch);
   cudaFree(c->sw_slot_new);
@@ -1007,6 +1078,7 @@ void psso_destroy(psso_ctx* c) {
 }
 
 int psso_bind(psso_ctx* c, const psso_buffers* b, void* stream) {
+  DEV_GUARD(c);
   if (!c) return fail(nullptr, PSSO_E_INVALID, "null context");
   if (!b || !b->sol || !b->pbests || !b->p_f || !b->gbest || !b->g_f)
     return fail(c, PSSO_E_INVALID, "sol, pbests, p_f, gbest and g_f buffers are required");
@@ -1031,6 +1103,7 @@ static int launch_init(psso_ctx* c) {
 }
 
 int psso_init(psso_ctx* c) {
+  DEV_GUARD(c);
   if (int rc = need_bound(c)) return rc;
   k_set_u64<<<1, 1, 0, c->stream>>>(c->bad, ~0ull);
   c->launches++;
@@ -1042,6 +1115,7 @@ int psso_init(psso_ctx* c) {
 }
 
 int psso_step(psso_ctx* c, int64_t t) {
+  DEV_GUARD(c);
   if (int rc = need_bound(c)) return rc;
   if (t < 0) return fail(c, PSSO_E_INVALID, "iteration must be >= 0");
   return fused_step(c, t, nullptr);
@@ -1070,6 +1144,7 @@ static int swarm_run(psso_ctx* c, int64_t t0, int64_t niter) {
   sp.traj = c->buf.traj;
   sp.traj_stride = 0;
   sp.g_f = c->buf.g_f;
+  sp.g_idx = c->g_idx;
   sp.gbest = c->buf.gbest;
   sp.seeds = c->sw_seed;
   sp.sol_f = c->buf.sol_f;
@@ -1119,6 +1194,7 @@ static int swarm_run(psso_ctx* c, int64_t t0, int64_t niter) {
 }
 
 int psso_run(psso_ctx* c, int64_t t0, int64_t niter) {
+  DEV_GUARD(c);
   if (int rc = need_bound(c)) return rc;
   if (t0 < 0 || niter < 0) return fail(c, PSSO_E_INVALID, "t0 and niter must be >= 0");
   if (niter == 0) return PSSO_OK;
@@ -1207,6 +1283,7 @@ static cudaError_t launch_seq(psso_ctx* c, int M, SeqParams q, int64_t B, cudaSt
 // run_sequential (core.py:213-258): one k_seq launch for the whole loop
 // (speculative passes with rollback, psso_seq.cuh).
 int psso_run_sequential(psso_ctx* c, int64_t t0, int64_t niter) {
+  DEV_GUARD(c);
   if (int rc = need_bound(c)) return rc;
   if (t0 < 0 || niter < 0) return fail(c, PSSO_E_INVALID, "t0 and niter must be >= 0");
   const psso_config* cfg = &c->cfg;
@@ -1241,6 +1318,7 @@ int psso_run_sequential(psso_ctx* c, int64_t t0, int64_t niter) {
   q.traj = c->buf.traj;
   q.traj_stride = 0;
   q.g_f = c->buf.g_f;
+  q.g_idx = c->g_idx;
   q.gbest = c->buf.gbest;
   q.seeds = c->seq_seed;
   q.sol_f = c->buf.sol_f;
@@ -1251,6 +1329,7 @@ int psso_run_sequential(psso_ctx* c, int64_t t0, int64_t niter) {
 }
 
 int psso_sequential_passes(psso_ctx* c, int64_t* passes) {
+  DEV_GUARD(c);
   if (!c || !passes) return fail(c, PSSO_E_INVALID, "null argument");
   *passes = 0;
   if (!c->seq_passes) return PSSO_OK;
@@ -1260,17 +1339,20 @@ int psso_sequential_passes(psso_ctx* c, int64_t* passes) {
 }
 
 int psso_search(psso_ctx* c, int64_t t) {
+  DEV_GUARD(c);
   if (int rc = need_bound(c)) return rc;
   return launch_tile(c, tile_params(c, M_SEARCH, t, nullptr));
 }
 
 int psso_evaluate(psso_ctx* c, int64_t t) {
+  DEV_GUARD(c);
   if (int rc = need_bound(c)) return rc;
   if (!c->buf.sol_f) return fail(c, PSSO_E_INVALID, "evaluate needs a sol_f buffer");
   return launch_tile(c, tile_params(c, M_LOAD | M_EVAL | M_SOLF, t < 0 ? -1 : t, nullptr));
 }
 
 int psso_update_pbests(psso_ctx* c) {
+  DEV_GUARD(c);
   if (int rc = need_bound(c)) return rc;
   if (!c->buf.sol_f) return fail(c, PSSO_E_INVALID, "update_pbests needs a sol_f buffer");
   const int64_t rows = c->cfg.row_hi - c->cfg.row_lo;
@@ -1287,6 +1369,7 @@ int psso_update_pbests(psso_ctx* c) {
 }
 
 int psso_update_gbest(psso_ctx* c) {
+  DEV_GUARD(c);
   if (int rc = need_bound(c)) return rc;
   const int64_t rows = c->cfg.row_hi - c->cfg.row_lo;
   k_argmin<<<c->argmin_grid, 256, 0, c->stream>>>(c->buf.p_f, rows, c->cfg.row_lo, c->slot_f, c->slot_i);
@@ -1300,7 +1383,7 @@ int psso_update_gbest(psso_ctx* c) {
 int64_t psso_candidate_bytes(const psso_config* cfg) {
   if (!cfg) return -1;
   const int64_t es = cfg->dtype == PSSO_F64 ? 8 : 4;
-  return 16 + ((cfg->nvar * es + 15) / 16) * 16;
+  return REC_HDR + ((cfg->nvar * es + 15) / 16) * 16;
 }
 
 static int local_cand(psso_ctx* c, void* cand, int nslots) {
@@ -1316,6 +1399,7 @@ static int local_cand(psso_ctx* c, void* cand, int nslots) {
 }
 
 int psso_init_local(psso_ctx* c, void* cand) {
+  DEV_GUARD(c);
   if (int rc = need_bound(c)) return rc;
   if (!cand) return fail(c, PSSO_E_INVALID, "null candidate buffer");
   k_set_u64<<<1, 1, 0, c->stream>>>(c->bad, ~0ull);
@@ -1326,6 +1410,7 @@ int psso_init_local(psso_ctx* c, void* cand) {
 }
 
 int psso_step_local(psso_ctx* c, int64_t t, void* cand) {
+  DEV_GUARD(c);
   if (int rc = need_bound(c)) return rc;
   if (!cand) return fail(c, PSSO_E_INVALID, "null candidate buffer");
   if (int rc = launch_fused(c, t, nullptr)) return rc;
@@ -1333,6 +1418,7 @@ int psso_step_local(psso_ctx* c, int64_t t, void* cand) {
 }
 
 int psso_apply_candidates(psso_ctx* c, int64_t t, const void* cands, int32_t ncand, int32_t is_init) {
+  DEV_GUARD(c);
   if (int rc = need_bound(c)) return rc;
   if (!cands || ncand < 1) return fail(c, PSSO_E_INVALID, "need at least one candidate record");
   GbParams g = gb_params(c, t, nullptr, is_init, 0);
@@ -1385,6 +1471,7 @@ int psso_p2p_close(void* dev_ptr) {
 
 int psso_publish_p2p(psso_ctx* c, const void* cand, void* const* peer_bufs, int32_t nranks,
                      int32_t rank, uint64_t epoch) {
+  DEV_GUARD(c);
   if (int rc = need_bound(c)) return rc;
   if (!cand || !peer_bufs || nranks < 1 || rank < 0 || rank >= nranks || epoch == 0)
     return fail(c, PSSO_E_INVALID, "bad p2p publish arguments");
@@ -1398,6 +1485,7 @@ int psso_publish_p2p(psso_ctx* c, const void* cand, void* const* peer_bufs, int3
 
 int psso_apply_p2p(psso_ctx* c, int64_t t, const void* my_buf, int32_t nranks, uint64_t epoch,
                    int32_t is_init) {
+  DEV_GUARD(c);
   if (int rc = need_bound(c)) return rc;
   if (!my_buf || nranks < 1 || epoch == 0) return fail(c, PSSO_E_INVALID, "bad p2p apply arguments");
   GbParams g = gb_params(c, t, nullptr, is_init, 0);
@@ -1414,6 +1502,7 @@ int psso_apply_p2p(psso_ctx* c, int64_t t, const void* my_buf, int32_t nranks, u
 }
 
 int psso_check(psso_ctx* c, int64_t* bad_t, int64_t* bad_i) {
+  DEV_GUARD(c);
   if (!c) return fail(nullptr, PSSO_E_INVALID, "null context");
   unsigned long long key = ~0ull;
   CK(c, cudaStreamSynchronize(c->stream));
@@ -1428,6 +1517,44 @@ int psso_check(psso_ctx* c, int64_t* bad_t, int64_t* bad_i) {
   return fail(c, PSSO_E_NONFINITE, "non-finite fitness");
 }
 
+int psso_nonfinite(psso_ctx* c, int64_t* bad_t, int64_t* bad_i, double* value) {
+  DEV_GUARD(c);
+  if (!c) return fail(nullptr, PSSO_E_INVALID, "null context");
+  int64_t bt = 0, bi = -1;
+  int rc = psso_check(c, &bt, &bi);
+  if (rc != PSSO_OK && rc != PSSO_E_NONFINITE) return rc;
+  double v = 0.0;
+  if (rc == PSSO_E_NONFINITE) {
+    if (c->bound && c->buf.sol_f && bi >= c->cfg.row_lo && bi < c->cfg.row_hi)
+      CK(c, cudaMemcpy(&v, c->buf.sol_f + (bi - c->cfg.row_lo), sizeof v, cudaMemcpyDeviceToHost));
+    else
+      CK(c, cudaMemcpy(&v, c->bad_val, sizeof v, cudaMemcpyDeviceToHost));
+  }
+  if (bad_t) *bad_t = bt;
+  if (bad_i) *bad_i = bi;
+  if (value) *value = v;
+  return rc;
+}
+
+int psso_result(psso_ctx* c, double* g_f, int64_t* g_idx, int64_t* bad_t, int64_t* bad_i) {
+  DEV_GUARD(c);
+  if (int rc = need_bound(c)) return rc;
+  CK(c, cudaStreamSynchronize(c->stream));
+  if (g_f) CK(c, cudaMemcpy(g_f, c->buf.g_f, sizeof(double), cudaMemcpyDeviceToHost));
+  if (g_idx) CK(c, cudaMemcpy(g_idx, c->g_idx, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  return psso_check(c, bad_t, bad_i);
+}
+
+int psso_set_gbest_index(psso_ctx* c, int64_t g_idx) {
+  DEV_GUARD(c);
+  if (int rc = need_bound(c)) return rc;
+  if (g_idx < -1 || g_idx >= c->cfg.nsol) return fail(c, PSSO_E_INVALID, "gBest index out of range");
+  k_set<<<1, 1, 0, c->stream>>>(c->g_idx, g_idx);
+  c->launches++;
+  CK(c, cudaGetLastError());
+  return PSSO_OK;
+}
+
 int64_t psso_launch_count(const psso_ctx* c) { return c ? c->launches : -1; }
 
 int psso_profile(psso_ctx* c, int32_t enable) {
@@ -1439,6 +1566,7 @@ int psso_profile(psso_ctx* c, int32_t enable) {
 }
 
 int psso_profile_read(psso_ctx* c, double* kernel_ms, int64_t* nlaunch) {
+  DEV_GUARD(c);
   if (!c) return fail(nullptr, PSSO_E_INVALID, "null context");
   CK(c, cudaStreamSynchronize(c->stream));
   double tot = 0.0;

@@ -54,6 +54,7 @@ struct SeqParams {
   unsigned long long* bad;  // [B]: min((t+1) << 40 | i) of the first non-finite fitness
   int64_t* passes;          // [B] passes run (diagnostic) or null
   int64_t rpc;              // rows per CTA of the cluster (multiple of 4)
+  int64_t* g_idx;           // [B] gBest particle index or null
 };
 
 // Shared memory (offsets in TileParams):
@@ -134,6 +135,7 @@ __global__ void __launch_bounds__(PSSO_SEQ_NT, 1)
     for (int64_t r = tid; r < r1 - r0; r += NTC) pf[r] = pfg[r0 + r];
   }
   double gf = q.g_f[b];
+  int64_t g_idx = q.g_idx ? q.g_idx[b] : -1;
   int64_t npass = 0;
   int par = 0;
   bool stop = false;
@@ -244,6 +246,7 @@ __global__ void __launch_bounds__(PSSO_SEQ_NT, 1)
           const T* src = cluster.map_shared_rank(pub_row, own) + par * D;
           for (int j = tid; j < D; j += NTC) gb[j] = src[j];
           gf = f;
+          g_idx = rs;
         }
       }
       __syncthreads();
@@ -265,6 +268,7 @@ __global__ void __launch_bounds__(PSSO_SEQ_NT, 1)
     for (int j = tid; j < D; j += NTC) gbp[j] = gb[j];
     if (tid == 0) {
       q.g_f[b] = gf;
+      if (q.g_idx) q.g_idx[b] = g_idx;
       if (q.passes) q.passes[b] = npass;
     }
   }

@@ -56,6 +56,7 @@ struct SwarmParams {
   double* sol_f;            // [B][rows] or null
   unsigned long long* bad;  // [B]
   unsigned long long* trace;  // PSSO_SWARM_TRACE builds: [niter][4] phase timestamps of CTA 0
+  int64_t* g_idx;           // [B] gBest particle index (parallel.py:208-211) or null
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -170,6 +171,7 @@ __global__ void __launch_bounds__(PSSO_SWARM_NT, 1)
   }
   double gf = sp.g_f[b];   // incumbent, identical in every thread of every CTA
   int64_t gi_inc = -1;     // incumbent particle (unknown at launch: first take copies)
+  int64_t g_idx = sp.g_idx ? sp.g_idx[b] : -1;  // the reported gBest index
   __syncthreads();
 
   unsigned int epoch = 0;
@@ -263,6 +265,7 @@ __global__ void __launch_bounds__(PSSO_SWARM_NT, 1)
         }
         gf = wf;
         gi_inc = wi;
+        g_idx = wi;
       }
       if (t >= 0 && c == 0 && tid == 0 && sp.traj) sp.traj[b * sp.traj_stride + t] = gf;  // :212
       const bool stop = red_n[NW] != 0;
@@ -317,6 +320,7 @@ __global__ void __launch_bounds__(PSSO_SWARM_NT, 1)
       }
       gf = wf;
       gi_inc = wi;
+      g_idx = wi;
     }
     if (t >= 0 && c == 0 && tid == 0 && sp.traj) sp.traj[b * sp.traj_stride + t] = gf;  // :212
     const bool stop = red_n[NW] != 0;
@@ -396,7 +400,10 @@ __global__ void __launch_bounds__(PSSO_SWARM_NT, 1)
   }
   if (c == 0) {  // the swarm's final gbest and g_f
     for (int j = tid; j < D; j += NTC) gbp[j] = gb[j];
-    if (tid == 0) sp.g_f[b] = gf;
+    if (tid == 0) {
+      sp.g_f[b] = gf;
+      if (sp.g_idx) sp.g_idx[b] = g_idx;
+    }
   }
   if constexpr (CL) cluster.sync();  // no CTA leaves while its smem may still be read
 }

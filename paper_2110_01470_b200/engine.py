@@ -141,14 +141,30 @@ class DeviceEngine:
 
     def check(self, init=False):
         """Raise NonFiniteFitnessError for the first non-finite fitness (core.py:190-193)."""
-        bt, bi = ctypes.c_int64(0), ctypes.c_int64(-1)
-        rc = self._lib.psso_check(self.ctx, ctypes.byref(bt), ctypes.byref(bi))
+        bt, bi, v = ctypes.c_int64(0), ctypes.c_int64(-1), ctypes.c_double()
+        rc = self._lib.psso_nonfinite(self.ctx, ctypes.byref(bt), ctypes.byref(bi), ctypes.byref(v))
         if rc == _lib.PSSO_E_NONFINITE:
-            local = bi.value - self.row_lo
-            value = float(self.sol_f[local].item())
             iteration = None if bt.value < 0 else int(bt.value)
-            raise NonFiniteFitnessError(value, int(bi.value), iteration)
+            raise NonFiniteFitnessError(float(v.value), int(bi.value), iteration)
         _lib.check(rc, self.ctx)
+
+    def result(self) -> tuple[float, int]:
+        """(g_f, gBest particle index) -- the argmin of parallel.py:208-211 / core.py:202.
+
+        Synchronizes; raises NonFiniteFitnessError like :meth:`check`."""
+        gf, gi = ctypes.c_double(), ctypes.c_int64(-1)
+        bt, bi = ctypes.c_int64(0), ctypes.c_int64(-1)
+        rc = self._lib.psso_result(self.ctx, ctypes.byref(gf), ctypes.byref(gi), ctypes.byref(bt),
+                                   ctypes.byref(bi))
+        if rc == _lib.PSSO_E_NONFINITE:
+            self.check()
+        _lib.check(rc, self.ctx)
+        return float(gf.value), int(gi.value)
+
+    @property
+    def best_index(self) -> int:
+        """Global index of the particle whose pBest row is gbest (-1 before initialization)."""
+        return self.result()[1]
 
     # -- sharded iteration (see sharded.py) -----------------------------------
     @property
@@ -186,9 +202,17 @@ class DeviceEngine:
                      sol_f=self.sol_f.cpu().numpy(), p_f=self.p_f.cpu().numpy(),
                      g_f=float(self.g_f.cpu()[0]))
 
-    def load(self, swarm: Swarm):
-        """Upload a host Swarm (any storage order) into this engine's buffers."""
+    def load(self, swarm: Swarm, best_index: int | None = None):
+        """Upload a host Swarm (any storage order) into this engine's buffers.
+
+        ``best_index``: the gBest particle (psso_result); default = the lowest
+        index whose p_f equals g_f (the parallel schedule's argmin), -1 if none.
+        """
         import torch
+
+        if best_index is None:
+            hit = np.flatnonzero(np.asarray(swarm.p_f) == swarm.g_f)
+            best_index = int(hit[0]) if hit.size else -1
 
         lo, hi = self.row_lo, self.row_hi
         tdt = self.sol.dtype
@@ -199,36 +223,52 @@ class DeviceEngine:
             self.sol_f.copy_(torch.as_tensor(np.ascontiguousarray(swarm.sol_f[lo:hi], dtype=np.float64)))
             self.p_f.copy_(torch.as_tensor(np.ascontiguousarray(swarm.p_f[lo:hi], dtype=np.float64)))
             self.g_f.fill_(float(swarm.g_f))
+        self._call("psso_set_gbest_index", int(best_index))
         self.stream.synchronize()
 
     # -- checkpoint / resume ---------------------------------------
+    def _identity(self) -> dict:
+        """Everything a checkpoint must match for a bitwise continuation."""
+        c = self.cfg
+        return {"seed": np.uint64(self.seed & _MASK64), "dtype": np.str_(self.dtype),
+                "rows": np.int64([self.row_lo, self.row_hi]), "fn_id": np.int64(c.fn_id),
+                "rng_mode": np.int64(c.rng_mode), "nsol": np.int64(c.nsol), "nvar": np.int64(c.nvar),
+                "thresholds": np.float64([c.cw, c.cp, c.cg]),
+                "box": np.float64([c.var_min, c.var_max])}
+
     def save_state(self, path, t_next: int) -> None:
         """Checkpoint the swarm before iteration ``t_next``.
 
         The keyed RNG makes ``(X, P, p_f, gbest, g_f, t)`` the whole state of a
         run (reference test_core.py:186-191: a shorter run is an exact prefix),
-        so a run restored from this file continues bit for bit.
+        so a run restored from this file continues bit for bit.  A run with a
+        pending non-finite fitness raises NonFiniteFitnessError instead of
+        being checkpointed.
         """
+        self.check()
+        g_f, g_idx = self.result()
         sw = self.to_host()
         np.savez(path, sol=sw.sol, pbests=sw.pbests, sol_f=sw.sol_f, p_f=sw.p_f, gbest=sw.gbest,
-                 g_f=np.float64(sw.g_f), t_next=np.int64(t_next), seed=np.uint64(self.seed & _MASK64),
-                 rows=np.int64([self.row_lo, self.row_hi]), dtype=np.str_(self.dtype),
-                 traj=self.traj.cpu().numpy())
+                 g_f=np.float64(g_f), g_idx=np.int64(g_idx), t_next=np.int64(t_next),
+                 traj=self.traj.cpu().numpy(), **self._identity())
 
     def restore_state(self, path) -> int:
-        """Load a checkpoint written by :meth:`save_state`; returns the next iteration."""
+        """Load a checkpoint written by :meth:`save_state`; returns the next iteration.
+
+        Rejects (ValueError) a checkpoint of another configuration: seed, dtype,
+        row range, objective, RNG mode, thresholds, box, nsol or nvar."""
         import torch
 
         z = np.load(path)
-        if (int(z["seed"]) != (self.seed & _MASK64) or str(z["dtype"]) != self.dtype
-                or list(z["rows"]) != [self.row_lo, self.row_hi]
-                or z["sol"].shape != tuple(self.sol.shape)):
-            raise ValueError("checkpoint does not match this engine (seed, dtype, rows or shape)")
+        want = self._identity()
+        bad = [k for k, v in want.items() if k not in z or not np.array_equal(z[k], v)]
+        if bad or z["sol"].shape != tuple(self.sol.shape):
+            raise ValueError("checkpoint does not match this engine ("
+                             + ", ".join(bad or ["shape"]) + ")")
         self.load(Swarm(sol=z["sol"], pbests=z["pbests"], gbest=z["gbest"], sol_f=z["sol_f"],
-                        p_f=z["p_f"], g_f=float(z["g_f"])))
+                        p_f=z["p_f"], g_f=float(z["g_f"])), best_index=int(z["g_idx"]))
         n = min(len(z["traj"]), self.traj.numel())
         with torch.cuda.stream(self.stream):
             self.traj[:n].copy_(torch.as_tensor(z["traj"][:n]))
         self.stream.synchronize()
         return int(z["t_next"])
-

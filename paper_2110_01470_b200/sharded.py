@@ -9,7 +9,7 @@ invariance (test_parallel.py:185-193).
 
 Per iteration each shard runs the fused kernel over its rows and reduces its
 own candidate record (p_f, global index, row); the records of all shards are
-gathered in rank order (one all-gather of R * (16 + D * sizeof(T)) bytes --
+gathered in rank order (one all-gather of R * (32 + D * sizeof(T)) bytes --
 the per-slice candidates + ``min(candidates)`` of parallel.py:199-208) and
 every shard applies the same deterministic selection (parallel.py:209-212).
 
@@ -122,9 +122,10 @@ class P2PExchange:
             self.world, self.ranks = dist.get_world_size(group), [dist.get_rank(group)]
         nbytes = int(self.L.psso_p2p_buffer_bytes(ctypes.byref(first.cfg), self.world))
         self.own = []
-        for _ in self.engines:
+        for e in self.engines:  # each buffer on its shard's device
             ptr = ctypes.c_void_p()
-            _lib.check(self.L.psso_p2p_alloc(nbytes, ctypes.byref(ptr)))
+            with torch.cuda.device(e.device):
+                _lib.check(self.L.psso_p2p_alloc(nbytes, ctypes.byref(ptr)))
             self.own.append(ptr.value)
         self.opened = []
         if not self.distributed:
@@ -143,7 +144,8 @@ class P2PExchange:
                     continue
                 ptr = ctypes.c_void_p()
                 buf = (ctypes.c_ubyte * self.HANDLE_BYTES).from_buffer_copy(hb)
-                _lib.check(self.L.psso_p2p_open(buf, ctypes.byref(ptr)))
+                with torch.cuda.device(first.device):
+                    _lib.check(self.L.psso_p2p_open(buf, ctypes.byref(ptr)))
                 self.opened.append(ptr.value)
                 table.append(ptr.value)
         self.table = torch.tensor(np.array(table, dtype=np.uint64).view(np.int64), device=first.device)

@@ -293,15 +293,37 @@ def test_checkpoint_resume_is_bitwise(schedule, dtype, tmp_path):
         assert np.array_equal(sb.sol, sc.sol) and np.array_equal(sb.pbests, sc.pbests)
         assert np.array_equal(sb.gbest, sc.gbest) and sb.g_f == sc.g_f
         assert np.array_equal(b.traj.cpu().numpy(), c.traj.cpu().numpy())
+        assert b.result() == c.result(), "gBest fitness and index survive the checkpoint"
     finally:
         b.close()
         c.close()
-    other = DeviceEngine(p, fn, 6, dtype=dtype)
+    import dataclasses
+
+    others = [(p, fn, 6, {}), (p, fn, 5, {"rng": "philox"}),
+              (dataclasses.replace(p, cg=0.9), fn, 5, {}),
+              (dataclasses.replace(p, var_min=-2.0), fn, 5, {})]
+    for q, f, seed, kw in others:  # another seed, RNG mode, thresholds, box
+        other = DeviceEngine(q, f, seed, dtype=dtype, **kw)
+        try:
+            with pytest.raises(ValueError, match="does not match"):
+                other.restore_state(tmp_path / "ck.npz")
+        finally:
+            other.close()
+
+
+def test_checkpoint_refuses_pending_nonfinite(tmp_path):
+    level = float(O.init_positions(0, 40, 4, -1.0, 1.0)[:, 0].max())  # init stays finite
+    fn = psso.probe_function(4, level=level, bounds=(-1.0, 1.0))
+    p = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=-1, var_max=1, nsol=40, nvar=4, niter=200)
+    eng = DeviceEngine(p, fn, 0)
     try:
-        with pytest.raises(ValueError, match="does not match"):
-            other.restore_state(tmp_path / "ck.npz")
+        eng.initialize()
+        eng.run(0, p.niter)
+        with pytest.raises(psso.NonFiniteFitnessError):
+            eng.save_state(tmp_path / "bad.npz", p.niter)
+        assert not (tmp_path / "bad.npz").exists()
     finally:
-        other.close()
+        eng.close()
 
 
 @pytest.mark.parametrize("fid,nsol,nvar", [("f5", 1024, 100), ("f7", 300, 77), ("f3", 200, 64)])

@@ -54,9 +54,9 @@ def test_struct_layouts_match_header():
     cfgp = ctypes.POINTER(_lib.PssoConfig)
     L = _lib.load()
     c = _lib.PssoConfig(fn_id=5, dtype=0, nvar=128)
-    assert L.psso_candidate_bytes(ctypes.byref(c)) == 16 + 128 * 8
+    assert L.psso_candidate_bytes(ctypes.byref(c)) == 32 + 128 * 8
     c32 = _lib.PssoConfig(fn_id=5, dtype=1, nvar=30)
-    assert L.psso_candidate_bytes(ctypes.byref(c32)) == 16 + 128
+    assert L.psso_candidate_bytes(ctypes.byref(c32)) == 32 + 128
     assert cfgp is not None
 
 

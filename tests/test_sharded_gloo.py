@@ -4,7 +4,7 @@ The product's ShardedDriver + ProcessGroupExchange (the code that runs over
 NCCL on the GPU box) drive per-rank shard engines through init, per-iteration
 candidate all-gathers and the gBest apply.  Here each rank's shard engine is
 the oracle (test infrastructure) packing the same candidate record layout the
-device writes (float64 p_f, int64 global index, the row) -- so the partition,
+device writes (float64 p_f, int64 global index, non-finite key and value, the row) -- so the partition,
 the exchange ordering and the record format are exercised end to end, and the
 result must equal the unsharded oracle run bit for bit (the reference's worker
 invariance, test_parallel.py:185-193).
@@ -30,7 +30,7 @@ class OracleShardEngine:
         self.lo, self.hi, self.D = lo, hi, nvar
         self.o = O.Oracle(fid, hi - lo, nvar, *thr, *bounds, seed, row_lo=lo)
         self.seed, self.bounds = seed, bounds
-        self.rec_bytes = 16 + ((nvar * 8 + 15) // 16) * 16
+        self.rec_bytes = 32 + ((nvar * 8 + 15) // 16) * 16
         self.traj = np.full(niter, np.nan)
         self.sw = None
 
@@ -41,8 +41,9 @@ class OracleShardEngine:
         buf = cand.numpy()
         buf[:8] = np.frombuffer(np.float64(f).tobytes(), np.uint8)
         buf[8:16] = np.frombuffer(np.int64(i).tobytes(), np.uint8)
+        buf[16:24] = 0xFF  # no non-finite fitness (the oracle raises instead)
         row = self.sw.pbests[i - self.lo]
-        buf[16:16 + 8 * self.D] = np.frombuffer(row.tobytes(), np.uint8)
+        buf[32:32 + 8 * self.D] = np.frombuffer(row.tobytes(), np.uint8)
 
     def init_local(self, cand):
         u = O.u_batch(self.seed, "INIT", 0, np.arange(self.lo, self.hi)[:, None],
@@ -64,7 +65,7 @@ class OracleShardEngine:
             f = float(np.frombuffer(r[:8].tobytes(), np.float64)[0])
             i = int(np.frombuffer(r[8:16].tobytes(), np.int64)[0])
             if best is None or (f, i) < best[:2]:
-                best = (f, i, np.frombuffer(r[16:16 + 8 * self.D].tobytes(), np.float64).copy())
+                best = (f, i, np.frombuffer(r[32:32 + 8 * self.D].tobytes(), np.float64).copy())
         if is_init or best[0] <= self.sw.g_f:
             self.sw.g_f = best[0]
             self.sw.gbest[:] = best[2]
