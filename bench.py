@@ -2,22 +2,29 @@
 """Benchmark of the fused PSSO iteration (BASELINE.json metric) -- one JSON line.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c3|c3f32|c4|c5|c2]
+                    [--workload c4|c3|c3f32|c5|c2|...] [--scaling strong|weak]
+                    [--exchange nccl|collective|p2p] [--rng reference|philox]
 
 A "step" is one PSSO iteration (search + evaluate + pBest + gBest) over the
-whole synthetic swarm.  Default workload = BASELINE config C3 (Rastrigin,
-N = 2^20 particles x Nvar = 128, fp64, reference keyed RNG: results
-bit-identical in positions/selections to the reference).  The swarm is the
-reference's own synthetic init (uniform in the box from the INIT stream).
+whole synthetic swarm.  Default workload = BASELINE config C4 (Rosenbrock,
+N = 2^24 particles x Nvar = 64, fp64, reference keyed RNG: positions,
+selections and fitness bit-identical to the reference), the config BASELINE
+quotes at 1/2/4/8 GPUs.  The swarm is the reference's own synthetic init
+(uniform in the box from the INIT stream).
 
-Under torchrun (N > 1) every rank owns a 2^20-particle shard (weak scaling,
-global N = 2^20 * ranks) and the ranks exchange gBest candidates through one
-NCCL all-gather per iteration; time = max over ranks of the device time.
+--gpus N > 1: one rank per GPU.  Without torchrun's WORLD_SIZE in the
+environment bench.py launches itself under torch.distributed.run with N ranks.
+Rank r owns the contiguous rows of the reference partition (parallel.py:147-
+149); per iteration the ranks exchange gBest candidate records -- by default
+through the library's own NCCL communicator, kernels and all-gather replayed
+from CUDA graphs (psso_run_sharded).  --scaling strong (default) keeps the
+workload's global N fixed (C4: 2^24 rows / N per GPU); weak gives every rank
+the workload's N.  Time = max over ranks of the device time.
 
 --impl reference times the reference algorithm on the host CPU cores: the C
 restatement in oracle/ (kind "port"; the reference itself is Python/numpy and
-is not shipped to the GPU box), all host threads, on a bounded sample of the
-workload's rows.
+is not shipped to the GPU box), all host threads, on the FULL workload when
+it fits in host memory (else a row sample, stated in the line).
 """
 
 from __future__ import annotations
@@ -136,67 +143,112 @@ def _dist():
     return ws, rank, local
 
 
-def cpu_baseline(fid, nvar, steps_budget_s=12.0, sample_rows=1 << 16, dtype="float64"):
-    """Oracle (C restatement, all host threads) on a bounded row sample; pvu/s."""
+BOXES = {"f1": (-5.12, 5.12), "f5": (-5.12, 5.12), "f4": (-2.048, 2.048), "f6": (-32.768, 32.768),
+         "f7": (-600.0, 600.0)}
+
+
+def _host_rows(nsol, nvar, want_full=True):
+    """Rows the host oracle can hold: the full workload when X, P (fp64) and the
+    oracle's temporaries fit in half the available host memory, else a sample."""
+    need = nsol * nvar * 8 * 2 + nsol * 8 * 4
+    avail = None
+    try:
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemAvailable:"):
+                avail = int(ln.split()[1]) * 1024
+    except OSError:
+        pass
+    if want_full and (avail is None or need <= avail // 2):
+        return nsol
+    per_row = nvar * 8 * 2 + 32
+    return max(1024, min(nsol, (avail // 2) // per_row if avail else 1 << 16))
+
+
+def cpu_baseline(fid, nsol, nvar, budget_s=12.0):
+    """Oracle (C restatement, all host threads) on the workload's own rows for ~budget_s; pvu/s."""
     from oracle import oracle as O
 
     threads = O.max_threads()
-    lo, hi = {"f1": (-5.12, 5.12), "f5": (-5.12, 5.12), "f4": (-2.048, 2.048),
-              "f6": (-32.768, 32.768)}[fid]
-    o = O.Oracle(fid, sample_rows, nvar, 0.3, 0.6, 0.8, lo, hi, 0, threads=threads)
+    rows = _host_rows(nsol, nvar)
+    lo, hi = BOXES[fid]
+    o = O.Oracle(fid, rows, nvar, 0.3, 0.6, 0.8, lo, hi, 0, threads=threads)
     sw = o.initialize()
-    o.run(sw, 0, 1)  # warm
     n, t0 = 0, time.perf_counter()
     while True:
-        o.run(sw, 1 + n, 1)
+        o.run(sw, n, 1)
         n += 1
         el = time.perf_counter() - t0
-        if el >= steps_budget_s or n >= 2000:
+        if el >= budget_s or n >= 2000:
             break
-    return {"value": sample_rows * nvar * n / el, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{sample_rows} of the workload's particles x Nvar={nvar}, {n} iterations "
-                      f"({el:.1f} s), oracle/psso_oracle.c with {threads} OpenMP threads"}
+    what = "all" if rows == nsol else f"{rows} of the"
+    return {"value": rows * nvar * n / el, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{what} {nsol} particles x Nvar={nvar}, {n} iterations ({el:.1f} s), "
+                      f"oracle/psso_oracle.c with {threads} OpenMP threads"}
+
+
+def _global_nsol(args, wl, ws):
+    fid, nsol, nvar, dtype, desc = WORKLOADS[wl]
+    return nsol * ws if args.scaling == "weak" else nsol
 
 
 def run_reference(args, wl):
     ws, rank, _ = _dist()
     if rank != 0:
         return
-    fid, nsol, nvar, dtype, desc = WORKLOADS[wl]
+    fid, _, nvar, dtype, desc = WORKLOADS[wl]
+    nsol = _global_nsol(args, wl, ws)
     from oracle import oracle as O
 
     threads = O.max_threads()
-    sample = min(nsol, 1 << 16) if nvar <= 256 else min(nsol, 1 << 11)
-    lo, hi = {"f1": (-5.12, 5.12), "f5": (-5.12, 5.12), "f4": (-2.048, 2.048),
-              "f6": (-32.768, 32.768)}[fid]
-    o = O.Oracle(fid, sample, nvar, 0.3, 0.6, 0.8, lo, hi, 0, threads=threads)
+    rows = _host_rows(nsol, nvar)
+    lo, hi = BOXES[fid]
+    o = O.Oracle(fid, rows, nvar, 0.3, 0.6, 0.8, lo, hi, 0, threads=threads)
     sw = o.initialize()
     o.run(sw, 0, args.warmup)
     t0 = time.perf_counter()
     o.run(sw, args.warmup, args.steps)
     el = time.perf_counter() - t0
-    value = sample * nvar * args.steps / el
+    value = rows * nvar * args.steps / el
+    full = rows == nsol
+    what = "the full workload" if full else f"a sample of {rows} of the {nsol} particles"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": el * 1e3 / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference INIT-stream swarm)",
-        "config": {"workload": desc + f" (host sample: {sample} particles)", "fn": fid,
-                   "nsol_sample": sample, "nvar": nvar, "l2": "n/a (CPU)"},
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference INIT-stream swarm, seed 0)",
+        "config": {"workload": desc + ("" if full else f" (host sample: {rows} particles)"),
+                   "fn": fid, "nsol": nsol, "nsol_host": rows, "nvar": nvar, "same_config": full,
+                   "l2": "n/a (CPU)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{sample} particles x Nvar={nvar} per step, oracle/psso_oracle.c "
-                                   f"(C restatement of the reference, numpy order) with {threads} threads"},
+                         "sample": f"{what} x Nvar={nvar} per step, oracle/psso_oracle.c (C "
+                                   f"restatement of the reference, numpy order) with {threads} threads"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def _max_over_ranks(vals, ws):
+    import torch.distributed as dist
+
+    if not dist.is_initialized():
+        return vals
+    import torch
+    import torch.distributed as dist
+
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor(vals, dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.cpu()]
 
 
 def run_ours(args, wl):
     import torch
 
     ws, rank, local = _dist()
-    fid, nsol_rank, nvar, dtype, desc = WORKLOADS[wl]
-    if ws > 1:
+    fid, _, nvar, dtype, desc = WORKLOADS[wl]
+    dist = None
+    sharded = ws > 1 or args.force_sharded
+    if sharded:
         import torch.distributed as dist
 
         # PSSO_BENCH_BACKEND=gloo (tests only): ranks may share a GPU, so the
@@ -213,67 +265,71 @@ def run_ours(args, wl):
     import paper_2110_01470_b200 as psso
     from paper_2110_01470_b200 import _lib
     from paper_2110_01470_b200.engine import DeviceEngine, make_config
-    from paper_2110_01470_b200.sharded import (P2PExchange, ProcessGroupExchange, ShardedDriver,
-                                               partition)
+    from paper_2110_01470_b200.sharded import (NcclExchange, P2PExchange, ProcessGroupExchange,
+                                               ShardedDriver, partition, run_parallel_distributed)
 
     fn = psso.make_function(fid, nvar)
-    nsol = nsol_rank * ws
+    nsol = _global_nsol(args, wl, ws)
     p = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=fn.var_min, var_max=fn.var_max,
-                       nsol=nsol, nvar=nvar, niter=args.warmup + args.steps + 1)
+                       nsol=nsol, nvar=nvar, niter=args.warmup + 2 * args.steps + 1)
     lo, hi = partition(nsol, ws)[rank]
     eng = DeviceEngine(p, fn, 0, dtype=dtype, rng=args.rng, row_lo=lo, row_hi=hi)
     L = _lib.load()
     es = 8 if dtype == "float64" else 4
-    if ws > 1:
+    drv = ex = None
+    if sharded:
         ex = (P2PExchange([eng], distributed=True) if args.exchange == "p2p"
-              else ProcessGroupExchange())
+              else NcclExchange(eng) if args.exchange == "nccl" else ProcessGroupExchange())
         drv = ShardedDriver([eng], ex, ws)
+
+    def run(t0, n):
+        if drv is not None:
+            with torch.cuda.stream(eng.stream):
+                drv.run(t0, n)
+        else:
+            eng.run(t0, n)
+
+    if drv is not None:
         with torch.cuda.stream(eng.stream):
             drv.initialize()
-            drv.run(0, args.warmup)
     else:
         eng.initialize()
-        eng.run(0, args.warmup)
+    run(0, args.warmup)
     torch.cuda.synchronize()
-    if ws > 1:
+    if sharded:
         dist.barrier()
 
-    # ---- timed region: K iterations, CUDA events on the engine's stream, kernel
-    # events around every fused tile launch (roofline), clocks sampled live
+    # ---- timed region: K iterations as the product runs them (graph-replayed
+    # iteration kernels, + the exchange for N > 1), CUDA events on the engine's
+    # stream, clocks sampled live; max over ranks
     sampler = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
     if sampler:
         sampler.start()
         time.sleep(0.3)
-    L.psso_profile(eng.ctx, 1)
     l0 = eng.launches
     start = torch.cuda.Event(enable_timing=True)
     stop = torch.cuda.Event(enable_timing=True)
     start.record(eng.stream)
-    if ws > 1:
-        with torch.cuda.stream(eng.stream):
-            drv.run(args.warmup, args.steps)
-    else:
-        eng.run(args.warmup, args.steps)
+    run(args.warmup, args.steps)
     stop.record(eng.stream)
     torch.cuda.synchronize()
-    if ws > 1:
+    if sharded:
         dist.barrier()
     launches = eng.launches - l0
-    kname = L.psso_kernel_name(eng.ctx).decode()
+    ms = start.elapsed_time(stop)
+    # ---- the iteration kernel's own duration: the same K iterations again with
+    # every iteration-kernel launch bracketed by CUDA events on the engine's
+    # stream (psso_profile: direct launches instead of the graph)
+    L.psso_profile(eng.ctx, 1)
+    run(args.warmup + args.steps, args.steps)
     kms, kn = ctypes.c_double(), ctypes.c_int64()
     _lib.check(L.psso_profile_read(eng.ctx, ctypes.byref(kms), ctypes.byref(kn)))
     L.psso_profile(eng.ctx, 0)
     clocks = sampler.stop() if sampler else None
     eng.check()
-    ms = start.elapsed_time(stop)
-    if ws > 1:
-        t = torch.tensor([ms, kms.value / max(kn.value, 1)], dtype=torch.float64,
-                         device="cuda" if dist.get_backend() == "nccl" else "cpu")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, kern_ms = float(t[0]), float(t[1])
-    else:
-        kern_ms = kms.value / max(kn.value, 1)  # per iteration
-    if ws > 1 and args.exchange == "p2p":
+    kname = L.psso_kernel_name(eng.ctx).decode()
+    ms, kern_ms = _max_over_ranks([ms, kms.value / max(kn.value, 1)], ws)
+    if sharded and args.exchange == "p2p":
         dist.barrier()  # every rank finished reading peer buffers before unmapping
         ex.close()
     eng.close()
@@ -287,86 +343,130 @@ def run_ours(args, wl):
     alg_bytes = 3 * es * rows_rank * nvar  # read X, read P, write X per pvu
     achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
 
-    # ---- e2e through the C ABI with host buffers (psso_solve = run_parallel)
-    e2e = None
-    if rank == 0:
-        cfg = make_config(psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=fn.var_min,
-                                         var_max=fn.var_max, nsol=nsol_rank, nvar=nvar,
-                                         niter=args.steps), fn, 0, dtype=dtype, rng=args.rng)
-        import numpy as np
+    # ---- e2e through the public API with host buffers: N = 1 psso_solve (C ABI:
+    # config in, trajectory + best position out); N > 1 every rank calls
+    # run_parallel_distributed (the multi-GPU public API) -- device allocation,
+    # init, K iterations, copy-back inside the wall-clock region; max over ranks
+    import numpy as np
 
+    cfg = make_config(psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=fn.var_min,
+                                     var_max=fn.var_max, nsol=nsol, nvar=nvar, niter=args.steps),
+                      fn, 0, dtype=dtype, rng=args.rng)
+    times = []
+    if not sharded:
         traj = np.empty(args.steps)
         best = np.empty(nvar, dtype=np.float64 if dtype == "float64" else np.float32)
         bf, wall = ctypes.c_double(), ctypes.c_double()
-        times = []
         for rep in range(4):  # first call warms module load / allocator; best of the other 3
             t0 = time.perf_counter()
             _lib.check(L.psso_solve(ctypes.byref(cfg), args.steps, traj.ctypes.data,
                                     best.ctypes.data, ctypes.byref(bf), ctypes.byref(wall)))
             times.append(time.perf_counter() - t0)
-        el = min(times[1:])
-        e2e = {"value": nsol_rank * nvar * args.steps / el, "unit": UNIT,
-               "h2d_bytes_per_step": ctypes.sizeof(cfg) / args.steps,
-               "d2h_bytes_per_step": (8 * args.steps + best.nbytes + 8) / args.steps,
-               "note": "psso_solve(config) -> host trajectory/best position; includes device "
-                       "alloc, init, all iterations and copy-back; the reference API takes no "
-                       "array inputs (the swarm is generated from the seed); best of 3 calls "
-                       "after a warm-up call (host-side API latency on the box varies; "
-                       "PSSO_SOLVE_TRACE=1 prints the phases)",
-               "calls_s": [round(x, 4) for x in times]}
-        if ws > 1:
-            e2e["note"] += "; measured on rank 0's shard size (single GPU)"
+        note = ("psso_solve(config) -> host trajectory/best position; includes device alloc, "
+                "init, all iterations and copy-back")
+    else:
+        pe = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=fn.var_min, var_max=fn.var_max,
+                            nsol=nsol, nvar=nvar, niter=args.steps)
+        ex_e2e = "collective" if args.exchange == "collective" else args.exchange
+        for rep in range(4):
+            dist.barrier()
+            t0 = time.perf_counter()
+            rec = run_parallel_distributed(pe, fn, 0, dtype=dtype, rng=args.rng, exchange=ex_e2e)
+            el = time.perf_counter() - t0
+            times.append(_max_over_ranks([el], ws)[0])
+            del rec
+        note = (f"run_parallel_distributed on every rank (exchange={ex_e2e}) -> host trajectory/"
+                "best position; includes device alloc, init, all iterations and copy-back; "
+                "max over ranks")
+    el = min(times[1:])
+    e2e = {"value": nsol * nvar * args.steps / el, "unit": UNIT,
+           "h2d_bytes_per_step": ctypes.sizeof(cfg) / args.steps,
+           "d2h_bytes_per_step": (8 * args.steps + es * nvar + 8) / args.steps,
+           "note": note + "; the reference API takes no array inputs (the swarm is generated "
+                          "from the seed); best of 3 calls after a warm-up call",
+           "calls_s": [round(x, 4) for x in times]}
 
     if rank != 0:
         dist.destroy_process_group()
         return
-    cpu = cpu_baseline(fid, nvar) if ws == 1 and not args.no_cpu else None
+    cpu = cpu_baseline(fid, nsol, nvar) if ws == 1 and not args.no_cpu else None
+    exch = {"nccl": " + library NCCL all-gather of gBest candidate records per iteration "
+                    "(CUDA-graph replayed)",
+            "collective": " + torch.distributed all-gather of gBest candidates per iteration",
+            "p2p": " + device-initiated P2P stores of gBest candidates per iteration"}[args.exchange]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64" if dtype == "float64" else "f32",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64" if dtype == "float64" else "f32",
         "data": "synthetic (reference INIT-stream swarm, seed 0)",
-        "config": {"workload": desc + (f" per rank, global N={nsol}" if ws > 1 else ""),
-                   "fn": fid, "nsol": nsol, "nvar": nvar, "rng": args.rng,
+        "config": {"workload": desc + (f", global N={nsol} over {ws} GPUs ({args.scaling} scaling)"
+                                       if ws > 1 else ""),
+                   "fn": fid, "nsol": nsol, "nsol_per_gpu": rows_rank, "nvar": nvar, "rng": args.rng,
                    "evals_per_s": nsol * args.steps / (ms * 1e-3),
                    "hbm_gbs_per_gpu": 3 * es * nsol * nvar * args.steps / (ms * 1e-3) / 1e9 / ws,
                    "l2": f"inputs larger than L2: X+P = {2 * es * rows_rank * nvar / 2**30:.2f} GiB "
                          f"per GPU vs 126 MB L2",
-                   "parallelism": f"particle shards x{ws}" + (
-                       (" + NCCL all-gather of gBest candidates per iteration" if args.exchange == "collective"
-                        else " + device-initiated P2P stores of gBest candidates per iteration")
-                       if ws > 1 else "")},
+                   "parallelism": f"particle shards x{ws}" + (exch if sharded else "")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": _traffic(wl, kname), "peak_source": peak_src,
                      "kernel": kname, "kernel_ms_per_iteration": kern_ms,
                      "alg_bytes_per_launch": alg_bytes, "alg_bytes_per_pvu": 3 * es,
-                     "note": ("per iteration: one fused launch (streaming path)" if "k_swarm" not in kname
-                              else "whole-run kernel: all timed iterations in one launch; L2/SMEM-"
-                                   "resident swarm, so the HBM roofline does not bind")},
+                     "note": ("iteration-kernel duration from CUDA events around every launch of "
+                              "a second K-iteration pass run right after the timed region "
+                              "(the timed region replays CUDA graphs, which take no per-launch "
+                              "events); max over ranks"
+                              if "k_swarm" not in kname else
+                              "whole-run kernel: all timed iterations in one launch; L2/SMEM-"
+                              "resident swarm, so the HBM roofline does not bind")},
         "gpu_launches": launches,
         "clocks": clocks,
         "e2e": e2e,
         "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
-    if ws > 1:
+    if sharded:
         dist.destroy_process_group()
+
+
+def _spawn(args):
+    """--gpus N > 1 without torchrun: relaunch this script with N ranks."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+           str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="N > 1: fixed global N (strong) or the workload's N per GPU (weak)")
     ap.add_argument("--rng", default="reference", choices=["reference", "philox"])
-    ap.add_argument("--exchange", default="collective", choices=["collective", "p2p"],
-                    help="N > 1: gBest records by NCCL all-gather or device-initiated P2P stores")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "collective", "p2p"],
+                    help="N > 1: gBest records by the library's NCCL all-gather in CUDA graphs, "
+                         "a torch.distributed all-gather, or device-initiated P2P stores")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg (diagnostics)")
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="tests: the multi-rank path (process group + exchange) even at one rank")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_spawn(args))
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws != args.gpus:
+        ap.error(f"--gpus {args.gpus} but WORLD_SIZE={ws}")
     if args.impl == "reference":
         run_reference(args, args.workload)
     else:

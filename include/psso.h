@@ -35,6 +35,7 @@ extern "C" {
 #define PSSO_E_CUDA 2        /* CUDA runtime failure */
 #define PSSO_E_NONFINITE 3   /* non-finite fitness -> NonFiniteFitnessError (core.py:43-53) */
 #define PSSO_E_UNSUPPORTED 4 /* shape/dtype outside what the kernels handle */
+#define PSSO_E_NCCL 5        /* NCCL failure (sharded iteration over a communicator) */
 
 /* dtype of the position matrices */
 #define PSSO_F64 0
@@ -156,6 +157,29 @@ int64_t psso_candidate_bytes(const psso_config* cfg);
 int psso_init_local(psso_ctx* ctx, void* cand);
 int psso_step_local(psso_ctx* ctx, int64_t t, void* cand);
 int psso_apply_candidates(psso_ctx* ctx, int64_t t, const void* cands, int32_t ncand, int32_t is_init);
+
+/* Sharded iteration over a communicator the library owns (one process per
+ * GPU; replaces the per-slice candidates + min() of parallel.py:199-212 across
+ * GPUs).  psso_nccl_unique_id: a 128-byte ncclUniqueId made on rank 0 and
+ * handed to every rank (e.g. over torch.distributed); psso_comm_create:
+ * collective ncclCommInitRank on the current device, rank `rank` of `nranks`
+ * (a session resource: create once, attach to every run's context);
+ * psso_attach_comm: the context (whose row range must be that rank's shard)
+ * borrows it until psso_destroy.  Then
+ * psso_init_sharded = initialize (core.py:196-210) over all shards, and
+ * psso_run_sharded = iterations t0..t0+niter-1, each: fused iteration kernel on
+ * the local rows -> this rank's candidate record -> ncclAllGather of the
+ * records over NVLink / NVSwitch -> k_apply (identical selection on every
+ * rank, trajectory[t]).  Iterations are replayed from a captured CUDA graph of
+ * 16 (kernels + collective), so the host issues one launch per 16 iterations.
+ * NCCL is resolved at run time (dlopen "libnccl.so.2", or PSSO_NCCL_LIB). */
+typedef struct psso_comm psso_comm;
+int psso_nccl_unique_id(void* id /* 128 bytes */);
+int psso_comm_create(const void* id, int32_t nranks, int32_t rank, psso_comm** out);
+void psso_comm_destroy(psso_comm* comm);
+int psso_attach_comm(psso_ctx* ctx, psso_comm* comm);  /* ctx borrows it */
+int psso_init_sharded(psso_ctx* ctx);
+int psso_run_sharded(psso_ctx* ctx, int64_t t0, int64_t niter);
 
 /* Device-initiated gBest exchange (replaces the NCCL all-gather of the
  * records; SURVEY §8 f #3).  Every rank owns an exchange buffer of

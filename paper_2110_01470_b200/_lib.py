@@ -18,6 +18,7 @@ PSSO_E_INVALID = 1
 PSSO_E_CUDA = 2
 PSSO_E_NONFINITE = 3
 PSSO_E_UNSUPPORTED = 4
+PSSO_E_NCCL = 5
 
 PSSO_F64 = 0
 PSSO_F32 = 1
@@ -36,7 +37,9 @@ EXPORTS = (
     "psso_kernel_name", "psso_solve_batch", "psso_p2p_buffer_bytes", "psso_p2p_alloc",
     "psso_p2p_free", "psso_p2p_handle", "psso_p2p_open", "psso_p2p_close", "psso_publish_p2p",
     "psso_apply_p2p", "psso_run_sequential", "psso_sequential_passes",
-    "psso_solve_sequential_batch",
+    "psso_solve_sequential_batch", "psso_nccl_unique_id", "psso_comm_create", "psso_comm_destroy",
+    "psso_attach_comm", "psso_init_sharded",
+    "psso_run_sharded",
 )
 
 
@@ -115,6 +118,13 @@ def load():
     L.psso_apply_candidates.argtypes = [vp, i64, vp, i32, i32]
     L.psso_check.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.psso_set_gbest_index.argtypes = [vp, i64]
+    L.psso_nccl_unique_id.argtypes = [vp]
+    L.psso_comm_create.argtypes = [vp, i32, i32, ctypes.POINTER(vp)]
+    L.psso_comm_destroy.argtypes = [vp]
+    L.psso_comm_destroy.restype = None
+    L.psso_attach_comm.argtypes = [vp, vp]
+    L.psso_init_sharded.argtypes = [vp]
+    L.psso_run_sharded.argtypes = [vp, i64, i64]
     L.psso_nonfinite.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(dbl)]
     L.psso_result.argtypes = [vp, ctypes.POINTER(dbl), ctypes.POINTER(i64), ctypes.POINTER(i64),
                               ctypes.POINTER(i64)]

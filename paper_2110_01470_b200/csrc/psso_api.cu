@@ -5,6 +5,8 @@
 // Reference anchors (/root/reference/pkg/src/sso/): run_parallel
 // parallel.py:152-233; phases parallel.py:120-144; initialize core.py:196-210;
 // RngStream.uniform rng.py:73-87; BenchmarkFn.__call__ benchmarks.py:86-94.
+#include <dlfcn.h>
+
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -30,6 +32,43 @@ constexpr int GRAPH_CHUNK = 16;  // iterations per captured graph
 #ifndef PSSO_SWARM_MAX_ELEMS
 #define PSSO_SWARM_MAX_ELEMS (1 << 22)  // N*D up to which psso_run uses the whole-run kernel
 #endif
+
+// NCCL, resolved at run time from the process (torch loads its bundled
+// libnccl.so.2; C callers put it on the library path or name it in
+// PSSO_NCCL_LIB), so libpsso.so has no link-time NCCL dependency.  Only the
+// five entry points the sharded iteration uses.
+struct NcclUid { char internal[128]; };  // ncclUniqueId (nccl.h NCCL_UNIQUE_ID_BYTES)
+struct NcclApi {
+  bool ok = false;
+  std::string err;
+  int (*get_unique_id)(NcclUid*) = nullptr;
+  int (*comm_init_rank)(void**, int, NcclUid, int) = nullptr;
+  int (*all_gather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
+  int (*comm_destroy)(void*) = nullptr;
+  const char* (*error_string)(int) = nullptr;
+};
+constexpr int NCCL_UINT8 = 1;  // ncclUint8
+
+const NcclApi& nccl() {
+  static NcclApi a = [] {
+    NcclApi r;
+    const char* env = std::getenv("PSSO_NCCL_LIB");
+    void* h = nullptr;
+    for (const char* name : {env, "libnccl.so.2", "libnccl.so"}) {
+      if (name && *name && (h = dlopen(name, RTLD_NOW | RTLD_GLOBAL)) != nullptr) break;
+    }
+    if (!h) { r.err = "libnccl.so.2 not found (import torch first or set PSSO_NCCL_LIB)"; return r; }
+    r.get_unique_id = (int (*)(NcclUid*))dlsym(h, "ncclGetUniqueId");
+    r.comm_init_rank = (int (*)(void**, int, NcclUid, int))dlsym(h, "ncclCommInitRank");
+    r.all_gather = (int (*)(const void*, void*, size_t, int, void*, cudaStream_t))dlsym(h, "ncclAllGather");
+    r.comm_destroy = (int (*)(void*))dlsym(h, "ncclCommDestroy");
+    r.error_string = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
+    r.ok = r.get_unique_id && r.comm_init_rank && r.all_gather && r.comm_destroy && r.error_string;
+    if (!r.ok) r.err = "libnccl lacks a required entry point";
+    return r;
+  }();
+  return a;
+}
 
 // Launch plan of the whole-run kernel (k_swarm); see plan_swarm.
 struct SwarmPlan {
@@ -182,6 +221,7 @@ struct GbParams {
   unsigned long long* bad;  // this shard's first non-finite key ((t+1) << 40 | i)
   const double* sol_f;      // this shard's sol_f (the non-finite value), may be null
   double* bad_val;          // value of the run's first non-finite fitness (sharded runs)
+  int64_t row_hi;           // one past this shard's last row
 };
 
 // Candidate record of a shard (psso_candidate_bytes): the exchange payload of
@@ -262,7 +302,7 @@ __global__ void __launch_bounds__(GB_THREADS) k_local_cand(const __grid_constant
     double v = 0.0;
     if (key != ~0ull) {
       const int64_t i = (int64_t)(key & ((1ull << 40) - 1));
-      if (g.sol_f && i >= g.row_lo) v = g.sol_f[i - g.row_lo];  // the owner's value
+      if (g.sol_f && i >= g.row_lo && i < g.row_hi) v = g.sol_f[i - g.row_lo];  // the owner's
       else if (g.bad_val) v = *g.bad_val;                       // learnt from an exchange
     }
     *reinterpret_cast<unsigned long long*>(rec + 16) = key;
@@ -464,6 +504,12 @@ __global__ void k_set_u64(unsigned long long* p, unsigned long long v) { *p = v;
 
 // ------------------------------------------------------------- context ----
 
+struct psso_comm {  // an NCCL communicator on one device (rank `rank` of `nranks`)
+  void* comm;
+  int32_t nranks, rank;
+  int device;
+};
+
 struct psso_ctx {
   psso_config cfg;
   psso_buffers buf;
@@ -513,6 +559,12 @@ struct psso_ctx {
   double* seq_pfn;       // rows scratch
   uint64_t* seq_seed;
   int64_t* seq_passes;
+  // sharded iteration over a library-owned NCCL communicator (psso_attach_nccl)
+  void* comm;            // ncclComm_t, borrowed from a psso_comm
+  int32_t nranks, rank;
+  unsigned char* cand;   // this rank's candidate record
+  unsigned char* gathered;  // [nranks] records, rank order
+  cudaGraphExec_t sgraph;   // GRAPH_CHUNK sharded iterations
   std::string kname;     // the iteration kernel psso_run launches (psso_kernel_name)
   std::string err;
 };
@@ -629,6 +681,7 @@ GbParams gb_params(psso_ctx* c, int64_t t, int64_t* t_dev, int is_init, int nslo
   g.bad = c->bad;
   g.sol_f = c->buf.sol_f;
   g.bad_val = c->bad_val;
+  g.row_hi = c->cfg.row_hi;
   return g;
 }
 
@@ -1055,6 +1108,10 @@ void psso_destroy(psso_ctx* c) {
   if (!c) return;
   DEV_GUARD(c);
   if (c->graph) cudaGraphExecDestroy(c->graph);
+  if (c->sgraph) cudaGraphExecDestroy(c->sgraph);
+  if (c->comm && c->stream) cudaStreamSynchronize(c->stream);  // the communicator is borrowed
+  cudaFree(c->cand);
+  cudaFree(c->gathered);
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   cudaFree(c->slot_f);
   cudaFree(c->slot_i);
@@ -1089,6 +1146,7 @@ int psso_bind(psso_ctx* c, const psso_buffers* b, void* stream) {
   c->stream = (cudaStream_t)stream;
   c->bound = true;
   if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }
+  if (c->sgraph) { cudaGraphExecDestroy(c->sgraph); c->sgraph = nullptr; }
   return PSSO_OK;
 }
 
@@ -1430,6 +1488,124 @@ int psso_apply_candidates(psso_ctx* c, int64_t t, const void* cands, int32_t nca
     k_apply<float><<<1, GB_THREADS, 0, c->stream>>>(g, (const unsigned char*)cands, rb, ncand);
   c->launches++;
   CK(c, cudaGetLastError());
+  return PSSO_OK;
+}
+
+// ---- sharded iteration over a library-owned NCCL communicator -----------
+int psso_nccl_unique_id(void* id) {
+  if (!id) return fail(nullptr, PSSO_E_INVALID, "null id buffer");
+  const NcclApi& n = nccl();
+  if (!n.ok) return fail(nullptr, PSSO_E_UNSUPPORTED, n.err);
+  NcclUid u;
+  const int r = n.get_unique_id(&u);
+  if (r) return fail(nullptr, PSSO_E_NCCL, std::string("ncclGetUniqueId: ") + n.error_string(r));
+  std::memcpy(id, &u, sizeof u);
+  return PSSO_OK;
+}
+
+int psso_comm_create(const void* id, int32_t nranks, int32_t rank, psso_comm** out) {
+  if (!out) return fail(nullptr, PSSO_E_INVALID, "null output pointer");
+  *out = nullptr;
+  if (!id || nranks < 1 || rank < 0 || rank >= nranks) return fail(nullptr, PSSO_E_INVALID, "bad communicator arguments");
+  const NcclApi& n = nccl();
+  if (!n.ok) return fail(nullptr, PSSO_E_UNSUPPORTED, n.err);
+  psso_comm* m = new psso_comm();
+  if (cudaGetDevice(&m->device) != cudaSuccess) { delete m; return fail(nullptr, PSSO_E_CUDA, "cudaGetDevice"); }
+  NcclUid u;
+  std::memcpy(&u, id, sizeof u);
+  const int r = n.comm_init_rank(&m->comm, nranks, u, rank);  // collective over the ranks
+  if (r) { delete m; return fail(nullptr, PSSO_E_NCCL, std::string("ncclCommInitRank: ") + n.error_string(r)); }
+  m->nranks = nranks;
+  m->rank = rank;
+  *out = m;
+  return PSSO_OK;
+}
+
+void psso_comm_destroy(psso_comm* m) {
+  if (!m) return;
+  if (m->comm) nccl().comm_destroy(m->comm);
+  delete m;
+}
+
+int psso_attach_comm(psso_ctx* c, psso_comm* m) {
+  DEV_GUARD(c);
+  if (int rc = need_bound(c)) return rc;
+  if (!m || !m->comm) return fail(c, PSSO_E_INVALID, "null communicator");
+  if (m->device != c->device) return fail(c, PSSO_E_INVALID, "communicator and context are on different devices");
+  const int64_t rb = psso_candidate_bytes(&c->cfg);
+  if (!c->cand) CK(c, cudaMalloc(&c->cand, (size_t)rb));
+  if (c->gathered && c->nranks != m->nranks) { cudaFree(c->gathered); c->gathered = nullptr; }
+  if (!c->gathered) CK(c, cudaMalloc(&c->gathered, (size_t)rb * m->nranks));
+  if (c->sgraph) { cudaGraphExecDestroy(c->sgraph); c->sgraph = nullptr; }
+  c->comm = m->comm;
+  c->nranks = m->nranks;
+  c->rank = m->rank;
+  return PSSO_OK;
+}
+
+// one exchange: this rank's record -> all-gather (NVLink / NVSwitch) -> apply
+static int sharded_exchange(psso_ctx* c, int64_t t, int64_t* t_dev, int is_init) {
+  const int64_t rb = psso_candidate_bytes(&c->cfg);
+  const int r = nccl().all_gather(c->cand, c->gathered, (size_t)rb, NCCL_UINT8, c->comm, c->stream);
+  if (r) return fail(c, PSSO_E_NCCL, std::string("ncclAllGather: ") + nccl().error_string(r));
+  GbParams g = gb_params(c, t, t_dev, is_init, 0);
+  if (is_init) g.traj = nullptr;
+  if (c->cfg.dtype == PSSO_F64)
+    k_apply<double><<<1, GB_THREADS, 0, c->stream>>>(g, c->gathered, rb, c->nranks);
+  else
+    k_apply<float><<<1, GB_THREADS, 0, c->stream>>>(g, c->gathered, rb, c->nranks);
+  c->launches++;
+  CK(c, cudaGetLastError());
+  return PSSO_OK;
+}
+
+int psso_init_sharded(psso_ctx* c) {
+  DEV_GUARD(c);
+  if (int rc = need_bound(c)) return rc;
+  if (!c->comm) return fail(c, PSSO_E_INVALID, "no communicator (psso_attach_comm)");
+  k_set_u64<<<1, 1, 0, c->stream>>>(c->bad, ~0ull);
+  c->launches++;
+  if (int rc = launch_init(c)) return rc;
+  if (int rc = local_cand(c, c->cand, c->chain ? c->init_grid : c->grid)) return rc;
+  return sharded_exchange(c, -1, nullptr, 1);
+}
+
+static int sharded_step(psso_ctx* c, int64_t t, int64_t* t_dev) {
+  if (int rc = launch_fused(c, t, t_dev)) return rc;
+  if (int rc = local_cand(c, c->cand, c->fused_grid)) return rc;
+  return sharded_exchange(c, t, t_dev, 0);
+}
+
+int psso_run_sharded(psso_ctx* c, int64_t t0, int64_t niter) {
+  DEV_GUARD(c);
+  if (int rc = need_bound(c)) return rc;
+  if (!c->comm) return fail(c, PSSO_E_INVALID, "no communicator (psso_attach_comm)");
+  if (t0 < 0 || niter < 0) return fail(c, PSSO_E_INVALID, "t0 and niter must be >= 0");
+  int64_t done = 0;
+  if (c->stream != nullptr && niter >= GRAPH_CHUNK && !c->profiling) {
+    if (!c->sgraph) {  // GRAPH_CHUNK x (fused kernel, record, all-gather, apply); t from t_dev
+      cudaGraph_t g;
+      CK(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+      const int64_t saved = c->launches;
+      for (int k = 0; k < GRAPH_CHUNK; ++k) {
+        int rc = sharded_step(c, 0, c->t_dev);
+        if (rc) { cudaStreamEndCapture(c->stream, &g); return rc; }
+      }
+      c->launches = saved;
+      CK(c, cudaStreamEndCapture(c->stream, &g));
+      cudaError_t e = cudaGraphInstantiate(&c->sgraph, g, 0);
+      cudaGraphDestroy(g);
+      if (e != cudaSuccess) return cuda_fail(c, e, "cudaGraphInstantiate (sharded)");
+    }
+    k_set<<<1, 1, 0, c->stream>>>(c->t_dev, t0);
+    c->launches++;
+    for (; done + GRAPH_CHUNK <= niter; done += GRAPH_CHUNK) {
+      CK(c, cudaGraphLaunch(c->sgraph, c->stream));
+      c->launches += 3 * GRAPH_CHUNK;
+    }
+  }
+  for (; done < niter; ++done)
+    if (int rc = sharded_step(c, t0 + done, nullptr)) return rc;
   return PSSO_OK;
 }
 

@@ -14,6 +14,13 @@ the per-slice candidates + ``min(candidates)`` of parallel.py:199-208) and
 every shard applies the same deterministic selection (parallel.py:209-212).
 
 Exchanges:
+  * ``NcclExchange``         -- the default across GPUs: the library owns an
+                                NCCL communicator (psso_comm) and runs
+                                whole chunks of iterations -- fused kernel,
+                                candidate record, ncclAllGather, apply -- from
+                                one captured CUDA graph per 16 iterations
+                                (psso_run_sharded): no host round trip per
+                                iteration.
   * ``LocalExchange``        -- all shards live in this process (virtual
                                 shards on one GPU); gather = concatenation.
   * ``ProcessGroupExchange`` -- one shard per process over torch.distributed
@@ -36,6 +43,8 @@ from .records import RunRecord, ScheduleKind
 
 __all__ = [
     "partition",
+    "NcclComm",
+    "NcclExchange",
     "LocalExchange",
     "ProcessGroupExchange",
     "P2PExchange",
@@ -51,6 +60,87 @@ def partition(nsol: int, parts: int) -> list[tuple[int, int]]:
         raise ValueError(f"parts must be >= 1, got {parts}")
     edges = np.linspace(0, nsol, parts + 1).astype(int)
     return [(int(a), int(b)) for a, b in zip(edges[:-1], edges[1:]) if b > a]
+
+
+class NcclComm:
+    """A library-owned NCCL communicator (psso_comm) for this process's rank and device.
+
+    Made once per (process group, device) and cached: creating a communicator
+    is a collective bootstrap costing far more than a run's iterations, so it
+    is a session resource like torch's process group.  The group is used once,
+    to hand rank 0's ncclUniqueId to every rank.
+    """
+
+    ID_BYTES = 128
+    _cache: dict = {}
+
+    def __init__(self, group, device):
+        import ctypes
+
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib
+
+        self.L = _lib.load()
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        uid = (ctypes.c_ubyte * self.ID_BYTES)()
+        if self.rank == 0:
+            _lib.check(self.L.psso_nccl_unique_id(uid))
+        box = [bytes(uid)]
+        src = dist.get_global_rank(group, 0) if group is not None else 0
+        dist.broadcast_object_list(box, src=src, group=group)
+        uid = (ctypes.c_ubyte * self.ID_BYTES).from_buffer_copy(box[0])
+        h = ctypes.c_void_p()
+        with torch.cuda.device(device):
+            _lib.check(self.L.psso_comm_create(uid, self.world, self.rank, ctypes.byref(h)))
+        self.handle = h
+
+    @classmethod
+    def get(cls, group, device):
+        key = (id(group), str(device))
+        if key not in cls._cache:
+            cls._cache[key] = cls(group, device)
+        return cls._cache[key]
+
+    def __del__(self):
+        try:
+            if self.handle:
+                self.L.psso_comm_destroy(self.handle)
+        except Exception:
+            pass
+
+
+class NcclExchange:
+    """Library-owned NCCL communicator; iterations run as graph-replayed device loops.
+
+    One shard per process (rank = rank in the torch.distributed ``group``).
+    The iteration path is psso_run_sharded: fused kernel, candidate record,
+    ncclAllGather and apply, captured in a CUDA graph of 16 iterations.
+    """
+
+    device_loop = True
+
+    def __init__(self, engine, group=None):
+        from . import _lib
+
+        self.L = _lib.load()
+        self.comm = NcclComm.get(group, engine.device)
+        self.world, self.rank = self.comm.world, self.comm.rank
+        _lib.check(self.L.psso_attach_comm(engine.ctx, self.comm.handle), engine.ctx)
+
+    def initialize(self, engines):
+        from . import _lib
+
+        for e in engines:
+            _lib.check(self.L.psso_init_sharded(e.ctx), e.ctx)
+
+    def run(self, engines, t0: int, niter: int):
+        from . import _lib
+
+        for e in engines:
+            _lib.check(self.L.psso_run_sharded(e.ctx, int(t0), int(niter)), e.ctx)
 
 
 class LocalExchange:
@@ -194,18 +284,27 @@ class ShardedDriver:
         return gathered
 
     def initialize(self):
-        for e, c in zip(self.engines, self.cands):
-            e.init_local(c)
-        self._exchange_and_apply(-1, True)
+        if getattr(self.exchange, "device_loop", False):
+            self.exchange.initialize(self.engines)
+        else:
+            for e, c in zip(self.engines, self.cands):
+                e.init_local(c)
+            self._exchange_and_apply(-1, True)
         for e in self.engines:
             e.check(init=True)
 
     def step(self, t: int):
+        if getattr(self.exchange, "device_loop", False):
+            self.exchange.run(self.engines, t, 1)
+            return
         for e, c in zip(self.engines, self.cands):
             e.step_local(t, c)
         self._exchange_and_apply(t, False)
 
     def run(self, t0: int, niter: int):
+        if getattr(self.exchange, "device_loop", False):
+            self.exchange.run(self.engines, t0, niter)  # graph-replayed on the device
+            return
         for t in range(t0, t0 + niter):
             self.step(t)
 
@@ -263,14 +362,16 @@ def run_virtual_shards(params: SsoParams, f, seed: int, shards: int, *, dtype="f
 
 
 def run_parallel_distributed(params: SsoParams, f, seed: int, *, group=None, dtype="float64",
-                             rng="reference", exchange: str = "collective") -> RunRecord:
+                             rng="reference", exchange: str = "nccl") -> RunRecord:
     """One shard per torch.distributed rank (one process per GPU, NCCL over NVLink).
 
     Every rank returns the same RunRecord.  ``wall_time_s`` is this rank's
     loop time; callers wanting the job time take the max over ranks.
-    ``exchange``: "collective" (all-gather over the process group) or "p2p"
-    (device-initiated stores into CUDA-IPC-mapped peer buffers; the group is
-    only used once, to exchange the IPC handles).
+    ``exchange``: "nccl" (default: the library's own communicator, iterations
+    replayed from CUDA graphs with the all-gather inside), "collective"
+    (all-gather over the torch process group, one host-issued exchange per
+    iteration; works over gloo) or "p2p" (device-initiated stores into
+    CUDA-IPC-mapped peer buffers; the group only exchanges the IPC handles).
     """
     import torch
     import torch.distributed as dist
@@ -283,7 +384,10 @@ def run_parallel_distributed(params: SsoParams, f, seed: int, *, group=None, dty
         raise ValueError(f"nsol={params.nsol} cannot give every one of {pg.world} ranks a particle")
     lo, hi = ranges[pg.rank]
     eng = DeviceEngine(params, f, seed, dtype=dtype, rng=rng, row_lo=lo, row_hi=hi)
-    ex = P2PExchange([eng], group=group, distributed=True) if exchange == "p2p" else pg
+    if exchange not in ("nccl", "collective", "p2p"):
+        raise ValueError(f"exchange must be 'nccl', 'collective' or 'p2p', got {exchange!r}")
+    ex = (P2PExchange([eng], group=group, distributed=True) if exchange == "p2p"
+          else NcclExchange(eng, group=group) if exchange == "nccl" else pg)
     try:
         drv = ShardedDriver([eng], ex, pg.world)
         with torch.cuda.stream(eng.stream):

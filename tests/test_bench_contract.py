@@ -32,6 +32,20 @@ def test_reference_arm_line():
     assert d["steps"] == 3 and d["warmup"] == 3 and d["n_gpus"] == 1
 
 
+def test_gpus_flag_spawns_its_own_ranks():
+    """--gpus 2 without torchrun: bench.py relaunches itself with 2 ranks (rank 0 prints)."""
+    d = _run("--impl", "reference", "--workload", "c1", "--gpus", "2", "--steps", "3",
+             "--warmup", "3")
+    assert d["n_gpus"] == 2 and d["impl"] == "reference" and d["scaling"] == "strong"
+    assert d["config"]["nsol"] == 100 and d["config"]["same_config"] is True
+
+
+def test_weak_scaling_grows_the_global_swarm():
+    d = _run("--impl", "reference", "--workload", "c1", "--gpus", "2", "--scaling", "weak",
+             "--steps", "3", "--warmup", "3")
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["config"]["nsol"] == 200
+
+
 def test_warmup_floor_enforced():
     out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--warmup", "2"],
                          capture_output=True, text=True, timeout=120, cwd=ROOT)
@@ -59,11 +73,41 @@ def test_bench_multi_rank_path_runs_under_torchrun(exchange):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"),
            "--gpus", "2", "--steps", "6", "--warmup", "3", "--workload", "c3sphere",
-           "--exchange", exchange]
+           "--exchange", exchange, "--no-cpu"]
     out = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [json.loads(ln) for ln in out.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1, out.stdout[-2000:]
     d = lines[0]
-    assert d["n_gpus"] == 2 and d["config"]["nsol"] == 2 * (1 << 20) and d["value"] > 0
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
+    assert d["config"]["nsol"] == 1 << 20 and d["config"]["nsol_per_gpu"] == 1 << 19
     assert d["gpu_launches"] > 0 and d["roofline"]["achieved"] > 0
+    assert d["e2e"]["value"] > 0 and len(d["e2e"]["calls_s"]) == 4
+
+
+@pytest.mark.gpu
+def test_bench_sharded_nccl_graph_path_world_size_1():
+    """torchrun with one rank and --force-sharded: the default multi-GPU path (library NCCL
+    communicator, kernels + all-gather replayed from CUDA graphs) on the C4 strong workload."""
+    import os
+    import socket
+
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"),
+           "--gpus", "1", "--steps", "20", "--warmup", "3", "--workload", "c4",
+           "--scaling", "strong", "--force-sharded", "--no-cpu"]
+    out = subprocess.run(cmd, cwd=ROOT, env=dict(os.environ), capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [json.loads(ln) for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = lines[0]
+    assert d["config"]["nsol"] == 1 << 24 and "NCCL" in d["config"]["parallelism"]
+    assert d["roofline"]["kernel"].startswith("k_chain") and d["roofline"]["frac"] > 0.5
+    assert d["e2e"]["value"] > 0
