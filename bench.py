@@ -241,6 +241,18 @@ def _max_over_ranks(vals, ws):
     return [float(x) for x in t.cpu()]
 
 
+def _sum_over_ranks(v, ws):
+    import torch
+    import torch.distributed as dist
+
+    if not dist.is_initialized():
+        return v
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.cpu()[0])
+
+
 def run_ours(args, wl):
     import torch
 
@@ -317,18 +329,31 @@ def run_ours(args, wl):
         dist.barrier()
     launches = eng.launches - l0
     ms = start.elapsed_time(stop)
-    # ---- the iteration kernel's own duration: the same K iterations again with
-    # every iteration-kernel launch bracketed by CUDA events on the engine's
-    # stream (psso_profile: direct launches instead of the graph)
+    clocks = sampler.stop() if sampler else None
+    # ---- the iteration kernel's duration over the timed region: the streaming
+    # kernels (k_chain, k_rows) time themselves on the device (first CTA start
+    # to last CTA end, %globaltimer) and count improved rows, per iteration,
+    # inside the graph replays (psso_iteration_stats)
+    sk_ms, s_imp, s_n = ctypes.c_double(), ctypes.c_int64(), ctypes.c_int64()
+    nstat = min(args.steps, 1024)
+    _lib.check(L.psso_iteration_stats(eng.ctx, args.warmup + args.steps - nstat, nstat,
+                                      ctypes.byref(sk_ms), ctypes.byref(s_imp), ctypes.byref(s_n)))
+    # ---- cross-check / fallback: the same K iterations again with every
+    # iteration-kernel launch bracketed by CUDA events on the engine's stream
+    # (psso_profile: direct launches instead of the graph)
     L.psso_profile(eng.ctx, 1)
     run(args.warmup + args.steps, args.steps)
     kms, kn = ctypes.c_double(), ctypes.c_int64()
     _lib.check(L.psso_profile_read(eng.ctx, ctypes.byref(kms), ctypes.byref(kn)))
     L.psso_profile(eng.ctx, 0)
-    clocks = sampler.stop() if sampler else None
     eng.check()
     kname = L.psso_kernel_name(eng.ctx).decode()
-    ms, kern_ms = _max_over_ranks([ms, kms.value / max(kn.value, 1)], ws)
+    dev_timed = s_n.value == nstat and nstat > 0
+    kern_dev = sk_ms.value / nstat if dev_timed else float("nan")
+    imp_rows = float(s_imp.value) if dev_timed else float("nan")
+    ms, kern_ev, kern_dev = _max_over_ranks([ms, kms.value / max(kn.value, 1), kern_dev], ws)
+    imp_rows = _sum_over_ranks(imp_rows, ws)
+    kern_ms = kern_dev if dev_timed else kern_ev
     if sharded and args.exchange == "p2p":
         dist.barrier()  # every rank finished reading peer buffers before unmapping
         ex.close()
@@ -342,6 +367,10 @@ def run_ours(args, wl):
     rows_rank = hi - lo
     alg_bytes = 3 * es * rows_rank * nvar  # read X, read P, write X per pvu
     achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
+    # rho: fraction of rows whose pBest improved, counted by the kernel;
+    # with it the pBest write-back (rho*T per pvu) and p_f traffic ((8 + 8 rho)/D)
+    rho = imp_rows / (nstat * nsol) if dev_timed else None
+    bpv_rho = (3 * es + rho * es + (8 + 8 * rho) / nvar) if rho is not None else None
 
     # ---- e2e through the public API with host buffers: N = 1 psso_solve (C ABI:
     # config in, trajectory + best position out); N > 1 every rank calls
@@ -411,13 +440,22 @@ def run_ours(args, wl):
                      "frac": achieved / peak, "traffic": _traffic(wl, kname), "peak_source": peak_src,
                      "kernel": kname, "kernel_ms_per_iteration": kern_ms,
                      "alg_bytes_per_launch": alg_bytes, "alg_bytes_per_pvu": 3 * es,
-                     "note": ("iteration-kernel duration from CUDA events around every launch of "
-                              "a second K-iteration pass run right after the timed region "
-                              "(the timed region replays CUDA graphs, which take no per-launch "
-                              "events); max over ranks"
-                              if "k_swarm" not in kname else
+                     "rho": rho, "bytes_per_pvu_with_rho": bpv_rho,
+                     "achieved_with_rho": (bpv_rho * rows_rank * nvar / (kern_ms * 1e-3) / 1e9
+                                           if bpv_rho is not None else None),
+                     "kernel_ms_events": kern_ev,
+                     "note": ("kernel_ms_per_iteration: the iteration kernel timed on the device "
+                              "(first CTA start to last CTA end, %globaltimer) for every iteration "
+                              "of the timed region, graph replays included (psso_iteration_stats); "
+                              "kernel_ms_events: CUDA events around every launch of a second "
+                              "K-iteration pass with direct launches; rho = improved rows / rows "
+                              "per iteration over the timed region, counted by the kernel; max "
+                              "over ranks" if dev_timed else
                               "whole-run kernel: all timed iterations in one launch; L2/SMEM-"
-                              "resident swarm, so the HBM roofline does not bind")},
+                              "resident swarm, so the HBM roofline does not bind"
+                              if "k_swarm" in kname else
+                              "kernel duration from CUDA events around every launch of a second "
+                              "K-iteration pass (this kernel records no device statistics)")},
         "gpu_launches": launches,
         "clocks": clocks,
         "e2e": e2e,

@@ -220,6 +220,16 @@ int psso_check(psso_ctx* ctx, int64_t* bad_t, int64_t* bad_i);
  * Returns PSSO_E_NONFINITE (outputs still written) if there was one. */
 int psso_result(psso_ctx* ctx, double* g_f, int64_t* g_idx, int64_t* bad_t, int64_t* bad_i);
 
+/* Per-iteration statistics the streaming iteration kernels (k_chain, k_rows)
+ * record on the device -- also inside graph replays: for iterations
+ * t0..t0+n-1 (n <= 1024, the most recent 1024 iterations are kept), the summed
+ * kernel duration (first CTA start to last CTA end, %globaltimer), the number
+ * of rows whose pBest improved (parallel.py:108-112; the rho of the roofline's
+ * pBest write-back bytes) and how many of the iterations were recorded
+ * (0 for kernels without statistics).  Synchronizes the stream. */
+int psso_iteration_stats(psso_ctx* ctx, int64_t t0, int64_t n, double* kernel_ms,
+                         int64_t* improved_rows, int64_t* timed_iterations);
+
 /* psso_check plus the non-finite fitness value (NonFiniteFitnessError.value,
  * core.py:43-53), also on shards that do not own the failing particle (the
  * value travels in the candidate records).  *value = 0 when there is none. */

@@ -222,7 +222,17 @@ struct GbParams {
   const double* sol_f;      // this shard's sol_f (the non-finite value), may be null
   double* bad_val;          // value of the run's first non-finite fitness (sharded runs)
   int64_t row_hi;           // one past this shard's last row
+  unsigned long long* stats;  // per-iteration kernel stats ring (iter_stats), may be null
 };
+
+// gBest kernels reset the stats slot of the next iteration (thread 0)
+__device__ __forceinline__ void reset_stats(unsigned long long* stats, int64_t t_next) {
+  if (!stats || t_next < 0) return;
+  unsigned long long* st = stats + 3 * (t_next & (STATS_CAP - 1));
+  st[0] = ~0ull;
+  st[1] = 0;
+  st[2] = 0;
+}
 
 // Candidate record of a shard (psso_candidate_bytes): the exchange payload of
 // parallel.py:199-208 plus the shard's non-finite state, so that every shard
@@ -278,6 +288,7 @@ __global__ void __launch_bounds__(GB_THREADS) k_gbest(const __grid_constant__ Gb
     const int64_t t = g.t_dev ? *g.t_dev : g.t_arg;
     if (g.traj && t >= 0) g.traj[t] = gf;
     if (g.t_dev) *g.t_dev = t + 1;
+    reset_stats(g.stats, t + 1);
   }
 }
 
@@ -359,6 +370,7 @@ __global__ void __launch_bounds__(GB_THREADS) k_apply(const __grid_constant__ Gb
     const int64_t t = g.t_dev ? *g.t_dev : g.t_arg;
     if (g.traj && t >= 0) g.traj[t] = gf;
     if (g.t_dev) *g.t_dev = t + 1;
+    reset_stats(g.stats, g.is_init ? 0 : t + 1);
   }
   __syncthreads();
   if (take_s) {
@@ -437,6 +449,7 @@ __global__ void __launch_bounds__(GB_THREADS) k_apply_p2p(const __grid_constant_
     if (take_s) *g.g_f = gf;
     if (take_s && g.g_idx) *g.g_idx = bi;
     if (g.traj && g.t_arg >= 0) g.traj[g.t_arg] = gf;
+    reset_stats(g.stats, g.is_init ? 0 : g.t_arg + 1);
     __threadfence_block();
   }
   __syncthreads();
@@ -535,6 +548,7 @@ struct psso_ctx {
   int64_t* t_dev;
   int64_t* g_idx;        // gBest particle index, -1 before initialization
   double* bad_val;       // first non-finite value learnt from a candidate exchange
+  unsigned long long* stats;  // per-iteration kernel stats ring [STATS_CAP][3]
   double* aux;
   uint64_t Kw, Kp, Kg, Kw32, Kp32, Kg32;
   int64_t launches;
@@ -651,6 +665,7 @@ TileParams tile_params(psso_ctx* c, int mode, int64_t t, const int64_t* t_dev, b
   p.pre = L.pre ? 1 : 0;
   p.div_n = make_div((uint32_t)L.plan.n);
   p.plan = L.plan;
+  p.stats = c->stats;
   return p;
 }
 
@@ -682,6 +697,7 @@ GbParams gb_params(psso_ctx* c, int64_t t, int64_t* t_dev, int is_init, int nslo
   g.sol_f = c->buf.sol_f;
   g.bad_val = c->bad_val;
   g.row_hi = c->cfg.row_hi;
+  g.stats = c->stats;
   return g;
 }
 
@@ -1069,10 +1085,19 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
       (e = cudaMalloc(&c->t_dev, sizeof(int64_t))) != cudaSuccess ||
       (e = cudaMalloc(&c->g_idx, sizeof(int64_t))) != cudaSuccess ||
       (e = cudaMalloc(&c->bad_val, sizeof(double))) != cudaSuccess ||
+      (e = cudaMalloc(&c->stats, 3 * STATS_CAP * sizeof(unsigned long long))) != cudaSuccess ||
       (e = cudaMemset(c->g_idx, 0xff, sizeof(int64_t))) != cudaSuccess ||
       (e = cudaMemset(c->bad, 0xff, sizeof(unsigned long long))) != cudaSuccess) {
     psso_destroy(c);
     return cuda_fail(nullptr, e, "psso_create alloc");
+  }
+  {
+    std::vector<unsigned long long> st(3 * STATS_CAP, 0ull);
+    for (int q = 0; q < STATS_CAP; ++q) st[3 * q] = ~0ull;
+    if ((e = cudaMemcpy(c->stats, st.data(), st.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess) {
+      psso_destroy(c);
+      return cuda_fail(nullptr, e, "psso_create stats");
+    }
   }
   if (c->swarm_fn) {
     const size_t es = cfg->dtype == PSSO_F64 ? 8 : 4;
@@ -1119,6 +1144,7 @@ void psso_destroy(psso_ctx* c) {
   cudaFree(c->t_dev);
   cudaFree(c->g_idx);
   cudaFree(c->bad_val);
+  cudaFree(c->stats);
   cudaFree(c->aux);
   cudaFree(c->sw_epoch);
   cudaFree(c->sw_slot_new);
@@ -1691,6 +1717,29 @@ int psso_check(psso_ctx* c, int64_t* bad_t, int64_t* bad_i) {
   if (bad_t) *bad_t = (int64_t)(key >> 40) - 1;
   if (bad_i) *bad_i = (int64_t)(key & ((1ull << 40) - 1));
   return fail(c, PSSO_E_NONFINITE, "non-finite fitness");
+}
+
+int psso_iteration_stats(psso_ctx* c, int64_t t0, int64_t n, double* kernel_ms, int64_t* improved,
+                         int64_t* timed) {
+  DEV_GUARD(c);
+  if (int rc = need_bound(c)) return rc;
+  if (t0 < 0 || n < 0 || n > STATS_CAP) return fail(c, PSSO_E_INVALID, "need 0 <= n <= 1024 iterations from t0 >= 0");
+  std::vector<unsigned long long> st(3 * STATS_CAP);
+  CK(c, cudaStreamSynchronize(c->stream));
+  CK(c, cudaMemcpy(st.data(), c->stats, st.size() * 8, cudaMemcpyDeviceToHost));
+  double ns = 0.0;
+  int64_t imp = 0, cnt = 0;
+  for (int64_t t = t0; t < t0 + n; ++t) {
+    const unsigned long long* q = &st[3 * (t & (STATS_CAP - 1))];
+    if (q[0] == ~0ull || q[1] < q[0]) continue;  // not recorded (kernel without stats)
+    ns += (double)(q[1] - q[0]);
+    imp += (int64_t)q[2];
+    ++cnt;
+  }
+  if (kernel_ms) *kernel_ms = ns * 1e-6;
+  if (improved) *improved = imp;
+  if (timed) *timed = cnt;
+  return PSSO_OK;
 }
 
 int psso_nonfinite(psso_ctx* c, int64_t* bad_t, int64_t* bad_i, double* value) {

@@ -108,8 +108,36 @@ struct TileParams {
   int32_t off_bar;             // k_fused: two mbarriers; stages start at off_xs
   int32_t stage_bytes;         // k_fused: bytes of one stage (X tile + P tile)
   int32_t pad3;
+  unsigned long long* stats;   // per-iteration ring [STATS_CAP][3] (see iter_stats) or null
   Plan plan;
 };
+
+// ---- per-iteration kernel statistics (psso_iteration_stats) ---------------
+// The streaming iteration kernels (k_chain, k_rows) record, per iteration t,
+// the launch's first CTA start and last CTA end (%globaltimer, ns) and the
+// number of rows whose pBest improved (parallel.py:108-112: the pBest
+// write-back bytes of the roofline's rho term).  Slot t & (STATS_CAP-1) is
+// reset by the gBest kernel of iteration t-1.  Recorded inside graph replays
+// too, where per-launch CUDA events cannot be.
+constexpr int STATS_CAP = 1024;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// whole CTA calls, after its last global store; nimp = this thread's improved rows
+__device__ __forceinline__ void iter_stats(unsigned long long* stats, int64_t t,
+                                           unsigned long long t_start, int nimp) {
+  if (!stats || t < 0) return;
+  unsigned long long* st = stats + 3 * (t & (STATS_CAP - 1));
+  const int w = __reduce_add_sync(0xffffffffu, (unsigned)nimp);
+  if ((threadIdx.x & 31) == 0 && w) atomicAdd(st + 2, (unsigned long long)w);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicMin(st, t_start);
+    atomicMax(st + 1, gtimer());
+  }
+}
 
 // ------------------------------------------------------------------ RNG ----
 
@@ -1062,7 +1090,7 @@ __device__ __forceinline__ const double* stage_aux(const double* aux, int D) {
 // store, fitness in numpy order, pbest/p_f/sol_f bookkeeping and the
 // lexicographic candidate.  The whole warp must call it (shuffles).
 template <typename T, int FN, int RNG, int M, bool INIT, bool FULL, bool RES = false>
-__device__ __forceinline__ void chain_step(const TileParams& p, const ChainEnv& ev, const T* gb,
+__device__ __forceinline__ bool chain_step(const TileParams& p, const ChainEnv& ev, const T* gb,
                                            const uint64_t* xg, T* scr, int64_t r, bool rv,
                                            T (&x)[M], const T (&pv)[M], double pf_row,
                                            double& best_f, int64_t& best_i, int& best_new) {
@@ -1248,6 +1276,7 @@ __device__ __forceinline__ void chain_step(const TileParams& p, const ChainEnv& 
   const double f = finish<T, FN>(s1, s2, prod, D, &x0, p.probe_level);
 
   // ---- bookkeeping (identical on the 8 lanes; lane k == 0 writes)
+  bool improved = false;
   if (rv) {
     if (k == 0) {
       if (!isfinite(f) && ev.bad)
@@ -1262,6 +1291,7 @@ __device__ __forceinline__ void chain_step(const TileParams& p, const ChainEnv& 
       const bool imp = f <= pf_row;  // parallel.py:109, ties refresh
       pf = imp ? f : pf_row;
       fresh_row = imp;
+      improved = imp;
       if (imp) {
         if (k == 0) ev.p_f[r] = f;
 #pragma unroll
@@ -1277,6 +1307,7 @@ __device__ __forceinline__ void chain_step(const TileParams& p, const ChainEnv& 
       best_new = fresh_row;
     }
   }
+  return improved;  // the row's pBest was rewritten (same on the segment's 8 lanes)
 }
 
 // Deterministic CTA argmin of the per-thread candidates -> slot (no atomics).
@@ -1320,6 +1351,7 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, PSSO_CHAIN_MINB)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = lane & 7;
   T* scr = reinterpret_cast<T*>(smem + p.off_scr) + warp * 4 * (8 * M);
+  const unsigned long long t_start = gtimer();
   if (!INIT && p.bad && *(volatile unsigned long long*)p.bad != ~0ull) return;
 
   ChainEnv ev;
@@ -1358,6 +1390,7 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, PSSO_CHAIN_MINB)
   const int64_t ngroups = (rows + 3) >> 2;
   double best_f = CUDART_INF;
   int64_t best_i = INT64_MAX;
+  int nimp = 0;
 
   // PF: each warp streams its next group of 4 rows (X and P) into a private
   // shared-memory buffer with TMA bulk copies while it computes the current
@@ -1431,10 +1464,12 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, PSSO_CHAIN_MINB)
       for (int m = 0; m < M; ++m) pv[m] = (T)0;
     }
     int best_new = 0;
-    chain_step<T, FN, RNG, M, INIT, FULL>(p, ev, gb, xg, scr, r, rv, x, pv, pf_row, best_f, best_i,
-                                          best_new);
+    const bool imp = chain_step<T, FN, RNG, M, INIT, FULL>(p, ev, gb, xg, scr, r, rv, x, pv, pf_row,
+                                                           best_f, best_i, best_new);
+    nimp += (imp && k == 0) ? 1 : 0;
   }
   cta_candidate<NW>(best_f, best_i, red_f, red_i, p.slot_f + blockIdx.x, p.slot_i + blockIdx.x);
+  if (!INIT) iter_stats(p.stats, ev.t, t_start, nimp);
 }
 
 // ---------------------------------------------------------------- k_rows ----
@@ -1473,6 +1508,7 @@ __global__ void __launch_bounds__(256, 2) k_rows(const __grid_constant__ TilePar
   const int k = lane & 7, s = lane >> 3;
   const int slot = warp / W, sw = warp % W;
   const int mode = M_SEARCH | M_EVAL | M_PBEST | M_CAND | (p.mode & M_SOLF);
+  const unsigned long long t_start = gtimer();
   if (p.bad && *(volatile unsigned long long*)p.bad != ~0ull) return;
   const int64_t t = p.t_dev ? *p.t_dev : p.t_arg;
   T* __restrict__ X = reinterpret_cast<T*>(p.X);
@@ -1516,6 +1552,7 @@ __global__ void __launch_bounds__(256, 2) k_rows(const __grid_constant__ TilePar
   double best_f = CUDART_INF;
   int64_t best_i = INT64_MAX;
   int round = 0;
+  int nimp = 0;
   for (int64_t r0 = (int64_t)blockIdx.x * RPC; r0 < rows; r0 += rstride, ++round) {  // CTA-uniform
     const int64_t r = r0 + slot;
     const bool rv = r < rows;
@@ -1617,6 +1654,7 @@ __global__ void __launch_bounds__(256, 2) k_rows(const __grid_constant__ TilePar
         if (p.sol_f && ((mode & M_SOLF) || !isfinite(f))) p.sol_f[r] = f;
         const double pf = imp ? f : pf_row;
         if (imp) p.p_f[r] = f;
+        nimp += imp ? 1 : 0;
         if (lex_less(pf, gi, best_f, best_i)) { best_f = pf; best_i = gi; }
       }
       if (imp) {  // this warp's slice of pbests[i] = sol[i], from registers
@@ -1641,6 +1679,7 @@ __global__ void __launch_bounds__(256, 2) k_rows(const __grid_constant__ TilePar
     p.slot_f[blockIdx.x] = best_f;
     p.slot_i[blockIdx.x] = best_i;
   }
+  iter_stats(p.stats, t, t_start, nimp);
 }
 
 }  // namespace psso

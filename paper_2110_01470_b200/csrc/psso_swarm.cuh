@@ -59,11 +59,6 @@ struct SwarmParams {
   int64_t* g_idx;           // [B] gBest particle index (parallel.py:208-211) or null
 };
 
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
 #ifndef PSSO_SWARM_TRACE
 #define PSSO_SWARM_TRACE 0
 #endif
