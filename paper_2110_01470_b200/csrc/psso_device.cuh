@@ -197,7 +197,16 @@ __device__ __forceinline__ double unit53(uint64_t h) {  // rng.py:87, exact
 
 struct Philox4 { uint32_t w[4]; };
 
-// Philox4x32-10 (Salmon et al. 2011); counter = (pair, i_lo, i_hi, t), key = seed.
+// Benchmark-mode keying: one Philox4x32-10 call per PAIR of coordinates
+// {16a + b, 16a + b + 8} (b < 8) of a particle -- the two coordinates one lane
+// of the chain mapping holds at m = 2a and 2a + 1 -- so each call's four words
+// serve two coordinates: word h = branch draw, word 2 + h = fresh draw of the
+// pair's half h (INIT: words 2h, 2h+1 = one 64-bit draw).
+// counter = (pair, i_lo, i_hi, t or 0xFFFFFFFF for INIT), key = seed.
+__device__ __forceinline__ uint32_t philox_pair(int j) { return (uint32_t)(((j >> 4) << 3) | (j & 7)); }
+__device__ __forceinline__ int philox_half(int j) { return (j >> 3) & 1; }
+
+// Philox4x32-10 (Salmon et al. 2011).
 __device__ __forceinline__ Philox4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2,
                                                  uint32_t c3, uint32_t k0, uint32_t k1) {
 #pragma unroll
@@ -571,6 +580,21 @@ __device__ void tile_fitness(const TileParams& p, const T* xsrc, int SX, T* buf,
 // lane needs it, so predication is free), and the cumulative thresholds turn
 // the select chain into three monotone compares:
 //   k >= Kw -> pbest, k >= Kp -> gbest, k >= Kg -> fresh   (else keep x)
+// The four-way select (core.py:160-173) from one half of a Philox pair:
+// branch word w[h] against the 32-bit thresholds, fresh = var_min + span * w[2+h] 2^-32.
+template <typename T>
+__device__ __forceinline__ T philox_select(const TileParams& p, const Philox4& w, int h, T x, T pb,
+                                           T gv) {
+  const uint32_t kb = h ? w.w[1] : w.w[0];
+  const double raw = __dmul_rn((double)(h ? w.w[3] : w.w[2]), 2.3283064365386963e-10);
+  const double fresh = __dadd_rn(p.var_min, __dmul_rn(p.span, raw));
+  T a = x;
+  a = kb >= p.Kw32 ? pb : a;
+  a = kb >= p.Kp32 ? gv : a;
+  a = kb >= p.Kg32 ? (T)fresh : a;
+  return a;
+}
+
 template <typename T, int V, int RNG>
 __device__ __forceinline__ VecT<T, V> search_chunk(const TileParams& p, const VecT<T, V>& x,
                                                    const VecT<T, V>& pb, const VecT<T, V>& gv,
@@ -591,21 +615,12 @@ __device__ __forceinline__ VecT<T, V> search_chunk(const TileParams& p, const Ve
       g += GAMMA;
     }
   } else {
-    Philox4 w;
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       const int j = col + v;
-      if (v == 0 || (j & 1) == 0)
-        w = philox4x32_10((uint32_t)(j >> 1), (uint32_t)gi, (uint32_t)(gi >> 32), (uint32_t)t,
-                          (uint32_t)seed, (uint32_t)(seed >> 32));
-      const uint64_t kb = w.w[j & 1];
-      const double raw = __dmul_rn((double)w.w[2 + (j & 1)], 2.3283064365386963e-10);
-      const double fresh = __dadd_rn(p.var_min, __dmul_rn(p.span, raw));
-      T a = x.v[v];
-      a = kb >= p.Kw32 ? pb.v[v] : a;
-      a = kb >= p.Kp32 ? gv.v[v] : a;
-      a = kb >= p.Kg32 ? (T)fresh : a;
-      nv.v[v] = a;
+      const Philox4 w = philox4x32_10(philox_pair(j), (uint32_t)gi, (uint32_t)(gi >> 32), (uint32_t)t,
+                                      (uint32_t)seed, (uint32_t)(seed >> 32));
+      nv.v[v] = philox_select<T>(p, w, philox_half(j), x.v[v], pb.v[v], gv.v[v]);
     }
   }
   return nv;
@@ -623,9 +638,9 @@ __device__ __forceinline__ VecT<T, V> init_chunk(const TileParams& p, uint64_t h
       h = mix64(hr ^ (GAMMA * (uint64_t)(col + v + 1)));
     } else {
       const int j = col + v;
-      Philox4 w = philox4x32_10((uint32_t)(j >> 1), (uint32_t)gi, (uint32_t)(gi >> 32),
+      Philox4 w = philox4x32_10(philox_pair(j), (uint32_t)gi, (uint32_t)(gi >> 32),
                                 0xFFFFFFFFu, (uint32_t)p.seed, (uint32_t)(p.seed >> 32));
-      const int s = (j & 1) * 2;
+      const int s = philox_half(j) * 2;
       h = ((uint64_t)w.w[s] << 32) | w.w[s + 1];
     }
     nv.v[v] = (T)__dadd_rn(p.var_min, __dmul_rn(p.span, unit53(h)));
@@ -1126,18 +1141,21 @@ __device__ __forceinline__ bool chain_step(const TileParams& p, const ChainEnv& 
     uint64_t hb = 0;
     if constexpr (RNG == 0) hb = fold64(ev.rootb, (uint64_t)gi);
     uint64_t g = GAMMA * (uint64_t)(k + 1);
+    Philox4 w;  // RNG 1: one call per pair (m even, m + 1), see philox_pair
 #pragma unroll
     for (int m = 0; m < M; ++m) {
       const int j = k + 8 * m;
+      if constexpr (RNG != 0) {
+        if ((m & 1) == 0)
+          w = philox4x32_10(philox_pair(j), (uint32_t)gi, (uint32_t)(gi >> 32), 0xFFFFFFFFu,
+                            (uint32_t)ev.seed, (uint32_t)(ev.seed >> 32));
+      }
       if (rv && (FULL || j < D)) {
         uint64_t h;
         if constexpr (RNG == 0) {
           h = mix64(hb ^ g);
         } else {
-          Philox4 w = philox4x32_10((uint32_t)(j >> 1), (uint32_t)gi, (uint32_t)(gi >> 32),
-                                    0xFFFFFFFFu, (uint32_t)ev.seed, (uint32_t)(ev.seed >> 32));
-          const int s2 = (j & 1) * 2;
-          h = ((uint64_t)w.w[s2] << 32) | w.w[s2 + 1];
+          h = (m & 1) ? (((uint64_t)w.w[2] << 32) | w.w[3]) : (((uint64_t)w.w[0] << 32) | w.w[1]);
         }
         const T v = (T)__dadd_rn(p.var_min, __dmul_rn(p.span, unit53(h)));
         st_row<T, RES>(pr + j, v);
@@ -1157,6 +1175,7 @@ __device__ __forceinline__ bool chain_step(const TileParams& p, const ChainEnv& 
       xb = xs30(fold64(ev.rootb, (uint64_t)gi));
       xf = xs30(fold64(ev.rootf, (uint64_t)gi));
     }
+    Philox4 w;  // RNG 1: one call per pair (m even, m + 1), see philox_pair
 #pragma unroll
     for (int m = 0; m < M; ++m) {
       const int j = k + 8 * m;
@@ -1164,6 +1183,11 @@ __device__ __forceinline__ bool chain_step(const TileParams& p, const ChainEnv& 
       // columns with a warp-uniform branch instead of computing and dropping them
       if (!FULL && 8 * m >= D) break;
       T v;
+      if constexpr (RNG != 0) {
+        if ((m & 1) == 0)
+          w = philox4x32_10(philox_pair(j), (uint32_t)gi, (uint32_t)(gi >> 32), (uint32_t)ev.t,
+                            (uint32_t)ev.seed, (uint32_t)(ev.seed >> 32));
+      }
       if constexpr (RNG == 0) {
         const uint64_t gx = xg[j];
         const uint64_t kb = mix64_tail<(M <= 8 || sizeof(T) == 8)>(xb ^ gx) >> 11;
@@ -1173,8 +1197,7 @@ __device__ __forceinline__ bool chain_step(const TileParams& p, const ChainEnv& 
         v = kb >= p.Kp ? gb[j] : v;
         v = kb >= p.Kg ? (T)fresh : v;
       } else {
-        VecT<T, 1> xv{{x[m]}}, pb{{pv[m]}}, gv{{gb[j]}};
-        v = search_chunk<T, 1, 1>(p, xv, pb, gv, 0, 0, j, (uint64_t)gi, ev.t, ev.seed).v[0];
+        v = philox_select<T>(p, w, m & 1, x[m], pv[m], gb[j]);
       }
       x[m] = v;
       if (rv && (FULL || j < D)) st_row<T, RES>(xr + j, v);
@@ -1607,11 +1630,14 @@ __global__ void __launch_bounds__(256, 2) k_rows(const __grid_constant__ TilePar
           accumulate(m, v);
         }
       } else {
+        Philox4 w;  // one call per pair (m even, m + 1): jb is k mod 16
 #pragma unroll
         for (int m = 0; m < M; ++m) {
           const int j = jb + 8 * m;
-          VecT<T, 1> xv{{x[m]}}, pb{{pv[m]}}, gv{{gbl[j]}};
-          x[m] = search_chunk<T, 1, 1>(p, xv, pb, gv, 0, 0, j, (uint64_t)gi, t, p.seed).v[0];
+          if ((m & 1) == 0)
+            w = philox4x32_10(philox_pair(j), (uint32_t)gi, (uint32_t)(gi >> 32), (uint32_t)t,
+                              (uint32_t)p.seed, (uint32_t)(p.seed >> 32));
+          x[m] = philox_select<T>(p, w, m & 1, x[m], pv[m], gbl[j]);
           stg_stream<T, 1>(xr + j, VecT<T, 1>{{x[m]}});
           accumulate(m, x[m]);
         }
