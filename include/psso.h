@@ -288,6 +288,13 @@ int psso_solve_sequential_batch(const psso_config* cfg, const uint64_t* seeds, i
                                 int64_t niter, double* traj, void* best_position,
                                 double* best_fitness, double* wall_s);
 
+/* The non-finite failure of this thread's last psso_solve_batch /
+ * psso_solve_sequential_batch (NonFiniteFitnessError's fields, core.py:43-53):
+ * the failing swarm's position in `seeds`, the iteration (-1 = initialization),
+ * the particle and the fitness value.  PSSO_E_NONFINITE if that call failed so,
+ * else PSSO_OK with *swarm = -1. */
+int psso_batch_failure(int64_t* swarm, int64_t* iteration, int64_t* particle, double* value);
+
 #ifdef __cplusplus
 }
 #endif

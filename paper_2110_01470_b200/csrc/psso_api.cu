@@ -26,6 +26,8 @@ using namespace psso;
 namespace {
 
 thread_local std::string g_err;
+struct BatchFailure { int64_t swarm = -1, t = 0, i = -1; double value = 0.0; };
+thread_local BatchFailure g_batch_fail;  // the last psso_solve_*batch non-finite failure
 
 constexpr int GB_THREADS = 256;
 constexpr int GRAPH_CHUNK = 16;  // iterations per captured graph
@@ -186,6 +188,11 @@ bool make_layout(int fn, int dtype, int64_t D, bool fused, Layout& L, std::strin
   L.off_bar = (int)o; o += 16;
   L.smem = o;
   return true;
+}
+
+// chain_row_stride<T, M>() (psso_device.cuh) for a runtime element size and M
+size_t host_row_stride(int es, int M) {
+  return (size_t)8 * M * es + (size_t)(es == 8 ? row_pad<double>() : row_pad<float>());
 }
 
 uint64_t k53(double c) {  // (h >> 11) * 2^-53 < c  <=>  (h >> 11) < ceil(c * 2^53)
@@ -650,6 +657,7 @@ TileParams tile_params(psso_ctx* c, int mode, int64_t t, const int64_t* t_dev, b
   p.span = c->cfg.var_max - c->cfg.var_min;
   p.span53 = std::ldexp(p.span, -53);
   p.span64 = std::ldexp(p.span, -64);
+  p.span32 = std::ldexp(p.span, -32);
   p.probe_level = c->cfg.probe_level;
   p.t_arg = t;
   p.t_dev = t_dev;
@@ -968,7 +976,7 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
         c->LF.off_bar = (int)align16((size_t)c->LF.off_red + 128 + 64 * M);
         c->LF.off_xs = (int)((c->LF.off_bar + 8 * nw + 127) & ~127);
         c->LF.off_scr = (int)align16((size_t)c->LF.off_xs +
-                                     (full && PSSO_CHAIN_PF ? (size_t)nw * 8 * (8 * M) * es : 0));
+                                     (full && PSSO_CHAIN_PF ? (size_t)nw * 8 * host_row_stride(es, M) : 0));
         c->LF.smem = (size_t)c->LF.off_scr + (smem_fn ? (size_t)nw * 4 * (8 * M) * es : 0);
         c->init_smem = c->LF.smem;
       }
@@ -993,7 +1001,7 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
       c->LF.off_flag = c->LF.off_leaf + (int)align16(2 * (size_t)(8 / W) * (8 * W + 1) * 8);
       c->LF.off_bar = (int)align16((size_t)c->LF.off_flag + 32);
       c->LF.off_xs = (int)((c->LF.off_bar + 64 + 127) & ~127);
-      c->LF.smem = (size_t)c->LF.off_xs + 8 * 8 * (size_t)128 * es;
+      c->LF.smem = (size_t)c->LF.off_xs + 8 * 8 * host_row_stride(es, 16);
     }
   }
   if (!c->tile_fn || !c->fused_fn) {
@@ -1967,11 +1975,11 @@ static int solve_batch(const psso_config* cfg, const uint64_t* seeds, int32_t ns
                             : fail(nullptr, PSSO_E_UNSUPPORTED, "no whole-run kernel for this batch");
   }
   const int G = pl.G;
-  struct Buf { void* p = nullptr; } X, P, pf, gb, gf, tr, ep, sf, si, sn, sr, sd, bad, xn, fn, pfn;
+  struct Buf { void* p = nullptr; } X, P, pf, gb, gf, tr, ep, sf, si, sn, sr, sd, bad, xn, fn, pfn, solf;
   cudaStream_t s = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   auto cleanup = [&]() {
-    for (Buf* b : {&X, &P, &pf, &gb, &gf, &tr, &ep, &sf, &si, &sn, &sr, &sd, &bad, &xn, &fn, &pfn})
+    for (Buf* b : {&X, &P, &pf, &gb, &gf, &tr, &ep, &sf, &si, &sn, &sr, &sd, &bad, &xn, &fn, &pfn, &solf})
       if (b->p) cudaFreeAsync(b->p, s);
     if (e0) cudaEventDestroy(e0);
     if (e1) cudaEventDestroy(e1);
@@ -1993,6 +2001,7 @@ static int solve_batch(const psso_config* cfg, const uint64_t* seeds, int32_t ns
       (e = pool_alloc(&sr.p, B * 2 * G * D * es, s)) != cudaSuccess ||
       (e = pool_alloc(&sd.p, B * 8, s)) != cudaSuccess ||
       (e = pool_alloc(&bad.p, B * 8, s)) != cudaSuccess ||
+      (e = pool_alloc(&solf.p, B * N * 8, s)) != cudaSuccess ||  // non-finite values
       (e = cudaMemcpyAsync(sd.p, seeds, B * 8, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
       (e = cudaMemsetAsync(bad.p, 0xff, B * 8, s)) != cudaSuccess) {
     cleanup();
@@ -2025,6 +2034,7 @@ static int solve_batch(const psso_config* cfg, const uint64_t* seeds, int32_t ns
   sp.gbest = gb.p;
   sp.seeds = (const uint64_t*)sd.p;
   sp.bad = (unsigned long long*)bad.p;
+  sp.sol_f = (double*)solf.p;
   auto launch = [&]() -> cudaError_t {
     cudaError_t r = cudaMemsetAsync(ep.p, 0, B * 2 * G * sizeof(unsigned int), s);
     if (r != cudaSuccess) return r;
@@ -2063,6 +2073,7 @@ static int solve_batch(const psso_config* cfg, const uint64_t* seeds, int32_t ns
     q.gbest = gb.p;
     q.seeds = (const uint64_t*)sd.p;
     q.bad = (unsigned long long*)bad.p;
+    q.sol_f = (double*)solf.p;
     cudaEventRecord(e0, s);
     if ((e = launch_seq(c, M, q, (int64_t)B, s)) != cudaSuccess) {
       cleanup();
@@ -2076,10 +2087,15 @@ static int solve_batch(const psso_config* cfg, const uint64_t* seeds, int32_t ns
   }
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) { cleanup(); return cuda_fail(nullptr, e, "psso_solve_batch"); }
   std::vector<unsigned long long> bk(B);
+  g_batch_fail = BatchFailure();
   e = cudaMemcpy(bk.data(), bad.p, B * 8, cudaMemcpyDeviceToHost);
   for (size_t q = 0; e == cudaSuccess && q < B; ++q)
     if (bk[q] != ~0ull) {
       const int64_t bt = (int64_t)(bk[q] >> 40) - 1, bi = (int64_t)(bk[q] & ((1ull << 40) - 1));
+      g_batch_fail.swarm = (int64_t)q;
+      g_batch_fail.t = bt;
+      g_batch_fail.i = bi;
+      cudaMemcpy(&g_batch_fail.value, (double*)solf.p + q * N + bi, 8, cudaMemcpyDeviceToHost);
       g_err = "non-finite fitness in swarm " + std::to_string(q) + " (seed " + std::to_string(seeds[q]) +
               ") at particle " + std::to_string(bi) +
               (bt < 0 ? std::string(" during initialization") : " at iteration " + std::to_string(bt));
@@ -2098,6 +2114,14 @@ static int solve_batch(const psso_config* cfg, const uint64_t* seeds, int32_t ns
 }
 
 extern "C" {
+
+int psso_batch_failure(int64_t* swarm, int64_t* iteration, int64_t* particle, double* value) {
+  if (swarm) *swarm = g_batch_fail.swarm;
+  if (iteration) *iteration = g_batch_fail.t;
+  if (particle) *particle = g_batch_fail.i;
+  if (value) *value = g_batch_fail.value;
+  return g_batch_fail.swarm >= 0 ? PSSO_E_NONFINITE : PSSO_OK;
+}
 
 int psso_solve_batch(const psso_config* cfg, const uint64_t* seeds, int32_t nseeds, int64_t niter,
                      double* traj, void* best_position, double* best_fitness, double* wall_s) {

@@ -96,6 +96,7 @@ struct TileParams {
   double var_min, span;
   double span53;               // span * 2^-53 (fresh = var_min + k * span53, exact rescale)
   double span64;               // span * 2^-64 (see fresh_offset)
+  double span32;               // span * 2^-32 (fp32 Philox fresh draw)
   double probe_level;
   int64_t t_arg;
   const int64_t* t_dev;        // if non-null, the iteration is read from here
@@ -582,16 +583,24 @@ __device__ void tile_fitness(const TileParams& p, const T* xsrc, int SX, T* buf,
 //   k >= Kw -> pbest, k >= Kp -> gbest, k >= Kg -> fresh   (else keep x)
 // The four-way select (core.py:160-173) from one half of a Philox pair:
 // branch word w[h] against the 32-bit thresholds, fresh = var_min + span * w[2+h] 2^-32.
+// fp32 (benchmark mode has no bitwise contract): the fresh draw in fp32,
+// var_min + w * (span 2^-32) in one FMA, instead of five fp64 operations.
 template <typename T>
 __device__ __forceinline__ T philox_select(const TileParams& p, const Philox4& w, int h, T x, T pb,
                                            T gv) {
   const uint32_t kb = h ? w.w[1] : w.w[0];
-  const double raw = __dmul_rn((double)(h ? w.w[3] : w.w[2]), 2.3283064365386963e-10);
-  const double fresh = __dadd_rn(p.var_min, __dmul_rn(p.span, raw));
+  const uint32_t wf = h ? w.w[3] : w.w[2];
+  T fresh;
+  if constexpr (sizeof(T) == 4) {
+    fresh = __fmaf_rn((float)wf, (float)p.span32, (float)p.var_min);
+  } else {
+    const double raw = __dmul_rn((double)wf, 2.3283064365386963e-10);
+    fresh = __dadd_rn(p.var_min, __dmul_rn(p.span, raw));
+  }
   T a = x;
   a = kb >= p.Kw32 ? pb : a;
   a = kb >= p.Kp32 ? gv : a;
-  a = kb >= p.Kg32 ? (T)fresh : a;
+  a = kb >= p.Kg32 ? fresh : a;
   return a;
 }
 
@@ -1055,12 +1064,25 @@ __device__ __forceinline__ T chain_term1(T x, T nb, int e) {
 #endif
 
 
-// Shared-memory row stride of the chain kernels' per-warp prefetch buffer:
-// dense rows, so each array of a group arrives with ONE bulk copy (the four
-// 8-lane segments then share banks: 2x the minimum LDS wavefronts, cheaper
-// than the issue cost of one copy per padded row).
+// Shared-memory row stride of the chain / rows kernels' per-warp prefetch
+// buffers.  The four 8-lane segments of a warp read the same columns of four
+// rows (or leaves): with dense rows (stride a multiple of 128 B) all four hit
+// the same banks -- 2x (fp64) / 4x (fp32) the minimum LDS wavefronts, 17 M /
+// 136 M conflicts per C3 / C4 launch.  PSSO_ROW_PAD=1 pads each row by half a
+// wavefront's width per segment (64 B fp64, 32 B fp32), which puts the
+// segments on disjoint banks at the price of one bulk copy per row instead of
+// one per group.  Measured (round 2, interleaved A/B): the padded
+// layout is SLOWER on every workload -- C3 0.551 vs 0.536-0.544 ms, C3 fp32
+// Philox 0.363 vs 0.342 ms, C4 5.29 vs 4.84 ms, C5 1.293 vs 1.276 ms -- the
+// four times more, four times smaller TMA copies cost more than the extra LDS
+// wavefronts, which the kernels hide.  Dense (0) is the default.
+#ifndef PSSO_ROW_PAD
+#define PSSO_ROW_PAD 0
+#endif
+template <typename T>
+__host__ __device__ constexpr int row_pad() { return PSSO_ROW_PAD ? (sizeof(T) == 8 ? 64 : 32) : 0; }
 template <typename T, int M>
-__host__ __device__ constexpr int chain_row_stride() { return 8 * M * (int)sizeof(T); }
+__host__ __device__ constexpr int chain_row_stride() { return 8 * M * (int)sizeof(T) + row_pad<T>(); }
 
 // Row store of the chain step: streaming global store, or a plain store when
 // the swarm is resident in shared memory (RES, k_swarm).
@@ -1428,10 +1450,20 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, PSSO_CHAIN_MINB)
   auto prefetch = [&](int64_t g) {  // whole warp calls; one lane issues both copies
     if (g >= ngroups) return;
     if (lane == 0) {
-      const uint32_t bytes = (uint32_t)(min((int64_t)4, rows - 4 * g) * 8 * M * sizeof(T));
-      mbar_expect_tx(wbar, 2 * bytes);
-      bulk_g2s(wbuf, reinterpret_cast<const T*>(p.X) + 4 * g * (int64_t)(8 * M), bytes, wbar);
-      bulk_g2s(wbuf + 4 * RS, reinterpret_cast<const T*>(p.P) + 4 * g * (int64_t)(8 * M), bytes, wbar);
+      const int nr = (int)min((int64_t)4, rows - 4 * g);
+      const uint32_t rb = (uint32_t)(8 * M * sizeof(T));
+      const T* xg0 = reinterpret_cast<const T*>(p.X) + 4 * g * (int64_t)(8 * M);
+      const T* pg0 = reinterpret_cast<const T*>(p.P) + 4 * g * (int64_t)(8 * M);
+      mbar_expect_tx(wbar, 2 * nr * rb);
+      if constexpr (row_pad<T>() == 0) {
+        bulk_g2s(wbuf, xg0, nr * rb, wbar);
+        bulk_g2s(wbuf + 4 * RS, pg0, nr * rb, wbar);
+      } else {
+        for (int q = 0; q < nr; ++q) {
+          bulk_g2s(wbuf + q * RS, xg0 + q * (8 * M), rb, wbar);
+          bulk_g2s(wbuf + (4 + q) * RS, pg0 + q * (8 * M), rb, wbar);
+        }
+      }
     }
   };
   if constexpr (PF) {
@@ -1561,8 +1593,16 @@ __global__ void __launch_bounds__(256, 2) k_rows(const __grid_constant__ TilePar
       constexpr uint32_t SB = (uint32_t)(512 * sizeof(T));  // bytes per slice
       mbar_expect_tx(wbar, 2 * SB);
       const int64_t off = row * (int64_t)D + 512 * sw;
-      bulk_g2s(wbuf, X + off, SB, wbar);
-      bulk_g2s(wbuf + 4 * RS, P + off, SB, wbar);
+      if constexpr (row_pad<T>() == 0) {
+        bulk_g2s(wbuf, X + off, SB, wbar);
+        bulk_g2s(wbuf + 4 * RS, P + off, SB, wbar);
+      } else {  // one copy per leaf, padded (see chain_row_stride)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          bulk_g2s(wbuf + q * RS, X + off + 128 * q, SB / 4, wbar);
+          bulk_g2s(wbuf + (4 + q) * RS, P + off + 128 * q, SB / 4, wbar);
+        }
+      }
     }
   };
   if (lane == 0) {

@@ -26,7 +26,7 @@ from typing import Optional, Sequence, Union
 import numpy as np
 
 from .benchmarks import BenchmarkFn, make_function
-from .core import SsoParams
+from .core import NonFiniteFitnessError, SsoParams
 from .core import run_sequential
 from .parallel import LayoutMode, run_parallel, run_parallel_batch, run_sequential_batch
 from .records import RunRecord, ScheduleKind
@@ -102,15 +102,20 @@ class SpeedupReport:
 
 @dataclass
 class ExperimentConfig:
-    """The reference's experiment configuration (harness.py:96-128).
+    """The reference's experiment configuration (harness.py:96-128), same fields and defaults.
 
-    Extra keyword fields: ``dtype`` and ``rng`` as in ``run_parallel``.
-    ``workers``, ``layout`` and ``block_size`` are accepted and have no effect
-    on results, as in the reference.
+    Extra keyword fields: ``dtype`` and ``rng`` as in ``run_parallel``, and
+    ``per_run_timing``: False (default) runs each cell's replications as one
+    batched device job and gives every record the batch's loop time divided by
+    the number of runs; True runs and times every replication on its own, the
+    reference's protocol (harness.py:148-163), for speedup / RE comparisons
+    (harness.py:354-384).  ``workers``, ``layout``, ``block_size`` and
+    ``parallel_cells`` are accepted and have no effect on results, as in the
+    reference (cells are already batched on the device).
     """
 
     functions: Sequence[Union[str, BenchmarkFn]] = ("f1",)
-    schedules: Sequence[ScheduleKind] = (ScheduleKind.PARALLEL,)
+    schedules: Sequence[ScheduleKind] = (ScheduleKind.SEQUENTIAL, ScheduleKind.PARALLEL)
     replications: int = 20
     base_seed: int = 0
     nsol: int = 100
@@ -122,9 +127,11 @@ class ExperimentConfig:
     workers: int = 1
     layout: LayoutMode = LayoutMode.PARTICLE_MAJOR
     record_trajectory: bool = False
+    parallel_cells: bool = False
     block_size: int = 1024
     dtype: str = "float64"
     rng: str = "reference"
+    per_run_timing: bool = False
 
     def __post_init__(self):
         if not self.functions:
@@ -168,7 +175,9 @@ def run_cell(fn: BenchmarkFn, config: ExperimentConfig, run_ids: Sequence[int],
                        niter=config.niter)
     seeds = [config.base_seed + rid for rid in run_ids]
     sequential = ScheduleKind(schedule) is ScheduleKind.SEQUENTIAL
-    if config.nvar <= 128 and config.nsol * config.nvar <= _BATCH_MAX_ELEMS:
+    batched = (not config.per_run_timing and config.nvar <= 128
+               and config.nsol * config.nvar <= _BATCH_MAX_ELEMS)
+    if batched:
         batch = run_sequential_batch if sequential else run_parallel_batch
         recs = batch(params, fn, seeds, dtype=config.dtype, rng=config.rng)
         per_run = recs[0].wall_time_s / len(recs)
@@ -242,7 +251,24 @@ def run_experiment(config: ExperimentConfig, out=None, summary_out=None) -> Expe
     try:
         for fn in functions:
             for schedule in config.schedules:
-                for rec in run_cell(fn, config, range(config.replications), schedule):
+                try:
+                    cell = run_cell(fn, config, range(config.replications), schedule)
+                except NonFiniteFitnessError:
+                    # a batched cell fails as a whole: replay it run by run so the
+                    # rows of the replications before the failing one are written
+                    # first, as the reference's sequential loop leaves them
+                    cell = []
+                    for rid in range(config.replications):
+                        try:
+                            one = run_cell(fn, replace(config, per_run_timing=True), [rid],
+                                           schedule)
+                        except NonFiniteFitnessError:
+                            for rec in cell:
+                                sink.add(rec)
+                                records.append(rec)
+                            raise
+                        cell.extend(one)
+                for rec in cell:
                     sink.add(rec)
                     records.append(rec)
     except BaseException as exc:
@@ -251,7 +277,10 @@ def run_experiment(config: ExperimentConfig, out=None, summary_out=None) -> Expe
     finally:
         sink.close()
     report = ExperimentReport(config=config, records=records, summaries=summarize(records),
-                              metadata={"block_size": config.block_size, "engine": "b200"})
+                              metadata={"block_size": config.block_size, "engine": "b200",
+                                        "wall_time_s": "per run (the reference protocol)"
+                                        if config.per_run_timing else
+                                        "batched cell: loop time of the batch / runs"})
     if summary_out is not None:
         write_summary(report.summaries, summary_out)
     return report

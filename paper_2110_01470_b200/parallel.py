@@ -274,13 +274,11 @@ def _solve_batch(params, f, seeds, dtype, rng, run_id_base, sequential) -> list:
     solve = L.psso_solve_sequential_batch if sequential else L.psso_solve_batch
     rc = solve(ctypes.byref(cfg), arr, B, n, traj.ctypes.data, best.ctypes.data,
                bestf.ctypes.data, ctypes.byref(wall))
-    if rc == _lib.PSSO_E_NONFINITE:  # "... at particle I (during initialization | at iteration T)"
-        import re
-
-        msg = _lib.last_error()
-        m = re.search(r"particle (\d+)(?: at iteration (\d+))?", msg)
-        it = None if m is None or m.group(2) is None else int(m.group(2))
-        raise NonFiniteFitnessError(float("nan"), int(m.group(1)) if m else -1, it)
+    if rc == _lib.PSSO_E_NONFINITE:  # the failing swarm's (iteration, particle, value)
+        sw, it, i, v = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_double()
+        L.psso_batch_failure(ctypes.byref(sw), ctypes.byref(it), ctypes.byref(i), ctypes.byref(v))
+        raise NonFiniteFitnessError(float(v.value), int(i.value),
+                                    None if it.value < 0 else int(it.value))
     _lib.check(rc)
     kind = ScheduleKind.SEQUENTIAL if sequential else ScheduleKind.PARALLEL
     return [

@@ -111,3 +111,61 @@ def test_run_experiment_both_schedules_match_reference_rows(tmp_path):
             assert a.best_fitness == b.best_fitness
         else:
             assert abs(a.best_fitness - b.best_fitness) <= 1e-12 * abs(b.best_fitness)
+
+
+def test_config_defaults_match_the_reference():
+    c = H.ExperimentConfig()
+    assert c.schedules == [ScheduleKind.SEQUENTIAL, ScheduleKind.PARALLEL]
+    assert H.ExperimentConfig(parallel_cells=True).parallel_cells is True  # accepted, no effect
+    assert c.per_run_timing is False
+
+
+@pytest.mark.gpu
+def test_failed_batched_cell_keeps_the_rows_of_earlier_runs(tmp_path):
+    """A non-finite fitness in replication k: rows 0..k-1 then '# FAILED' (reference
+    harness.py:217-263 writes each run as it completes)."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2110_01470_b200 as P
+
+    from oracle import oracle as O
+
+    # probe objective: +inf once x[0] exceeds the level.  With the oracle, the
+    # largest x[0] each seed reaches (initialization and iteration 0); the level is
+    # seed 0's, so the first seed that goes above it fails and the earlier ones do not
+    def reach(seed):
+        o = O.Oracle("f1", 8, 4, 0.3, 0.6, 0.8, -1.0, 1.0, seed)
+        sw = o.initialize()
+        m = sw.sol[:, 0].max()
+        o.search(sw, 0)
+        return max(m, sw.sol[:, 0].max())
+
+    level = reach(0)
+    k = next((s for s in range(1, 12) if reach(s) > level), None)
+    if k is None:
+        pytest.skip("no seed exceeds seed 0's reach")
+    fn = P.probe_function(4, level=level, bounds=(-1.0, 1.0))
+    cfg = H.ExperimentConfig(functions=[fn], schedules=[ScheduleKind.PARALLEL], replications=12,
+                             nsol=8, nvar=4, niter=1)
+    out = tmp_path / "r.csv"
+    with pytest.raises(P.NonFiniteFitnessError):
+        H.run_experiment(cfg, out=out)
+    lines = out.read_text().splitlines()
+    rows = [ln for ln in lines[1:] if not ln.startswith("#")]
+    assert lines[-1].startswith("# FAILED: NonFiniteFitnessError")
+    assert len(rows) == k, (k, rows)
+
+
+@pytest.mark.gpu
+def test_per_run_timing_protocol():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    cfg = H.ExperimentConfig(functions=["f1"], schedules=[ScheduleKind.PARALLEL], replications=3,
+                             nsol=50, nvar=10, niter=20, per_run_timing=True)
+    rep = H.run_experiment(cfg)
+    batched = H.run_experiment(H.ExperimentConfig(**{**cfg.__dict__, "per_run_timing": False}))
+    assert [r.best_fitness for r in rep.records] == [r.best_fitness for r in batched.records]
+    assert rep.metadata["wall_time_s"].startswith("per run")
+    assert len({r.wall_time_s for r in rep.records}) == 3  # each run timed on its own
