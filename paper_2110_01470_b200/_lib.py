@@ -32,7 +32,7 @@ EXPORTS = (
     "psso_init", "psso_step", "psso_run", "psso_search", "psso_evaluate",
     "psso_update_pbests", "psso_update_gbest", "psso_candidate_bytes", "psso_init_local",
     "psso_step_local", "psso_apply_candidates", "psso_check", "psso_result", "psso_set_gbest_index", "psso_nonfinite",
-    "psso_iteration_stats", "psso_batch_failure",
+    "psso_iteration_stats", "psso_batch_failure", "psso_run_p2p",
     "psso_launch_count",
     "psso_rng_uniform", "psso_eval_rows", "psso_solve", "psso_profile", "psso_profile_read",
     "psso_kernel_name", "psso_solve_batch", "psso_p2p_buffer_bytes", "psso_p2p_alloc",
@@ -119,6 +119,7 @@ def load():
     L.psso_apply_candidates.argtypes = [vp, i64, vp, i32, i32]
     L.psso_check.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.psso_set_gbest_index.argtypes = [vp, i64]
+    L.psso_run_p2p.argtypes = [vp, i64, i64, vp, vp, i32, i32]
     L.psso_batch_failure.argtypes = [ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64),
                                      ctypes.POINTER(dbl)]
     L.psso_iteration_stats.argtypes = [vp, i64, i64, ctypes.POINTER(dbl), ctypes.POINTER(i64),

@@ -405,10 +405,17 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned 
   return v;
 }
 
+// Graph-replayed loops take the epoch from the device iteration counter:
+// epoch = t + 2 (initialization: 1), so a captured graph needs no host value.
+__device__ __forceinline__ unsigned long long p2p_epoch(unsigned long long epoch, const int64_t* t_dev) {
+  return t_dev ? (unsigned long long)(*t_dev + 2) : epoch;
+}
+
 __global__ void __launch_bounds__(GB_THREADS) k_publish(const unsigned char* cand,
                                                         unsigned char* const* bufs, int R, int rank,
-                                                        unsigned long long epoch, int64_t rec_bytes,
-                                                        int64_t flag_bytes) {
+                                                        unsigned long long epoch_arg, int64_t rec_bytes,
+                                                        int64_t flag_bytes, const int64_t* t_dev) {
+  const unsigned long long epoch = p2p_epoch(epoch_arg, t_dev);
   const uint64_t* src = reinterpret_cast<const uint64_t*>(cand);
   const int64_t words = rec_bytes / 8;
   const int slot = (int)(epoch & 1) * R + rank;  // records double-buffered by epoch parity
@@ -427,10 +434,11 @@ __global__ void __launch_bounds__(GB_THREADS) k_publish(const unsigned char* can
 template <typename T>
 __global__ void __launch_bounds__(GB_THREADS) k_apply_p2p(const __grid_constant__ GbParams g,
                                                           const unsigned char* buf, int R,
-                                                          unsigned long long epoch, int64_t rec_bytes,
+                                                          unsigned long long epoch_arg, int64_t rec_bytes,
                                                           int64_t flag_bytes) {
   __shared__ int winner;
   __shared__ int take_s;
+  const unsigned long long epoch = p2p_epoch(epoch_arg, g.t_dev);
   // a rank can publish epoch e+1 before a slower rank applied epoch e, never
   // e+2 (that needs the slower rank's e+1 record): parity buffers suffice
   const int par = (int)(epoch & 1);
@@ -455,8 +463,10 @@ __global__ void __launch_bounds__(GB_THREADS) k_apply_p2p(const __grid_constant_
     const double gf = take_s ? bf : inc;
     if (take_s) *g.g_f = gf;
     if (take_s && g.g_idx) *g.g_idx = bi;
-    if (g.traj && g.t_arg >= 0) g.traj[g.t_arg] = gf;
-    reset_stats(g.stats, g.is_init ? 0 : g.t_arg + 1);
+    const int64_t t = g.t_dev ? *g.t_dev : g.t_arg;
+    if (g.traj && t >= 0) g.traj[t] = gf;
+    if (g.t_dev) *g.t_dev = t + 1;
+    reset_stats(g.stats, g.is_init ? 0 : t + 1);
     __threadfence_block();
   }
   __syncthreads();
@@ -586,6 +596,10 @@ struct psso_ctx {
   unsigned char* cand;   // this rank's candidate record
   unsigned char* gathered;  // [nranks] records, rank order
   cudaGraphExec_t sgraph;   // GRAPH_CHUNK sharded iterations
+  cudaGraphExec_t pgraph;   // GRAPH_CHUNK P2P-exchange iterations (psso_run_p2p)
+  const void* pg_peers;     // the arguments pgraph was captured with
+  const void* pg_buf;
+  int32_t pg_R, pg_rank;
   std::string kname;     // the iteration kernel psso_run launches (psso_kernel_name)
   std::string err;
 };
@@ -1142,6 +1156,7 @@ void psso_destroy(psso_ctx* c) {
   DEV_GUARD(c);
   if (c->graph) cudaGraphExecDestroy(c->graph);
   if (c->sgraph) cudaGraphExecDestroy(c->sgraph);
+  if (c->pgraph) cudaGraphExecDestroy(c->pgraph);
   if (c->comm && c->stream) cudaStreamSynchronize(c->stream);  // the communicator is borrowed
   cudaFree(c->cand);
   cudaFree(c->gathered);
@@ -1181,6 +1196,7 @@ int psso_bind(psso_ctx* c, const psso_buffers* b, void* stream) {
   c->bound = true;
   if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }
   if (c->sgraph) { cudaGraphExecDestroy(c->sgraph); c->sgraph = nullptr; }
+  if (c->pgraph) { cudaGraphExecDestroy(c->pgraph); c->pgraph = nullptr; }
   return PSSO_OK;
 }
 
@@ -1687,7 +1703,8 @@ int psso_publish_p2p(psso_ctx* c, const void* cand, void* const* peer_bufs, int3
     return fail(c, PSSO_E_INVALID, "bad p2p publish arguments");
   const int64_t rb = psso_candidate_bytes(&c->cfg);
   k_publish<<<1, GB_THREADS, 0, c->stream>>>((const unsigned char*)cand, (unsigned char* const*)peer_bufs,
-                                             nranks, rank, epoch, rb, (int64_t)align16((size_t)nranks * 16));
+                                             nranks, rank, epoch, rb, (int64_t)align16((size_t)nranks * 16),
+                                             nullptr);
   c->launches++;
   CK(c, cudaGetLastError());
   return PSSO_OK;
@@ -1708,6 +1725,69 @@ int psso_apply_p2p(psso_ctx* c, int64_t t, const void* my_buf, int32_t nranks, u
     k_apply_p2p<float><<<1, GB_THREADS, 0, c->stream>>>(g, (const unsigned char*)my_buf, nranks, epoch, rb, fb);
   c->launches++;
   CK(c, cudaGetLastError());
+  return PSSO_OK;
+}
+
+// one P2P exchange step with t (and the epoch) from the device counter
+static int p2p_step_dev(psso_ctx* c, const void* peer_bufs, const void* my_buf, int32_t nranks,
+                        int32_t rank) {
+  if (int rc = launch_fused(c, 0, c->t_dev)) return rc;
+  if (int rc = local_cand(c, c->cand, c->fused_grid)) return rc;
+  const int64_t rb = psso_candidate_bytes(&c->cfg), fb = (int64_t)align16((size_t)nranks * 16);
+  k_publish<<<1, GB_THREADS, 0, c->stream>>>(c->cand, (unsigned char* const*)peer_bufs, nranks, rank, 0,
+                                             rb, fb, c->t_dev);
+  GbParams g = gb_params(c, 0, c->t_dev, 0, 0);
+  if (c->cfg.dtype == PSSO_F64)
+    k_apply_p2p<double><<<1, GB_THREADS, 0, c->stream>>>(g, (const unsigned char*)my_buf, nranks, 0, rb, fb);
+  else
+    k_apply_p2p<float><<<1, GB_THREADS, 0, c->stream>>>(g, (const unsigned char*)my_buf, nranks, 0, rb, fb);
+  c->launches += 2;
+  CK(c, cudaGetLastError());
+  return PSSO_OK;
+}
+
+int psso_run_p2p(psso_ctx* c, int64_t t0, int64_t niter, void* const* peer_bufs, const void* my_buf,
+                 int32_t nranks, int32_t rank) {
+  DEV_GUARD(c);
+  if (int rc = need_bound(c)) return rc;
+  if (!peer_bufs || !my_buf || nranks < 1 || rank < 0 || rank >= nranks || t0 < 0 || niter < 0)
+    return fail(c, PSSO_E_INVALID, "bad p2p loop arguments");
+  if (!c->cand) CK(c, cudaMalloc(&c->cand, (size_t)psso_candidate_bytes(&c->cfg)));
+  if (c->pgraph && (c->pg_peers != peer_bufs || c->pg_buf != my_buf || c->pg_R != nranks || c->pg_rank != rank)) {
+    cudaGraphExecDestroy(c->pgraph);
+    c->pgraph = nullptr;
+  }
+  if (niter == 0) return PSSO_OK;
+  k_set<<<1, 1, 0, c->stream>>>(c->t_dev, t0);
+  c->launches++;
+  int64_t done = 0;
+  const bool graph = c->stream != nullptr && !c->profiling;
+  if (graph && niter >= GRAPH_CHUNK) {
+    if (!c->pgraph) {  // GRAPH_CHUNK x (fused kernel, record, publish, apply)
+      cudaGraph_t gr;
+      CK(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+      const int64_t saved = c->launches;
+      for (int k = 0; k < GRAPH_CHUNK; ++k) {
+        int rc = p2p_step_dev(c, peer_bufs, my_buf, nranks, rank);
+        if (rc) { cudaStreamEndCapture(c->stream, &gr); return rc; }
+      }
+      c->launches = saved;
+      CK(c, cudaStreamEndCapture(c->stream, &gr));
+      cudaError_t e = cudaGraphInstantiate(&c->pgraph, gr, 0);
+      cudaGraphDestroy(gr);
+      if (e != cudaSuccess) return cuda_fail(c, e, "cudaGraphInstantiate (p2p)");
+      c->pg_peers = peer_bufs;
+      c->pg_buf = my_buf;
+      c->pg_R = nranks;
+      c->pg_rank = rank;
+    }
+    for (; done + GRAPH_CHUNK <= niter; done += GRAPH_CHUNK) {
+      CK(c, cudaGraphLaunch(c->pgraph, c->stream));
+      c->launches += 4 * GRAPH_CHUNK;
+    }
+  }
+  for (; done < niter; ++done)  // same kernels, launched directly
+    if (int rc = p2p_step_dev(c, peer_bufs, my_buf, nranks, rank)) return rc;
   return PSSO_OK;
 }
 

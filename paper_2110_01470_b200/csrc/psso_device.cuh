@@ -1059,6 +1059,9 @@ __device__ __forceinline__ T chain_term1(T x, T nb, int e) {
 #ifndef PSSO_CHAIN_MINB
 #define PSSO_CHAIN_MINB 2
 #endif
+#ifndef PSSO_CHAIN_MINB_F32
+#define PSSO_CHAIN_MINB_F32 PSSO_CHAIN_MINB  // resident CTAs per SM for the fp32 chain kernels
+#endif
 #ifndef PSSO_CHAIN_PF
 #define PSSO_CHAIN_PF 1  // FULL iteration kernel: TMA prefetch of the next group
 #endif
@@ -1383,7 +1386,7 @@ __device__ __forceinline__ void cta_candidate(double best_f, int64_t best_i, dou
 //   off_xs     per-warp prefetch buffers (FULL iteration kernel): [X 4 rows][P 4 rows]
 //   off_scr    per-warp smem rows [4][8M] (f3, f7, f8)
 template <typename T, int FN, int RNG, int M, bool INIT, bool FULL>
-__global__ void __launch_bounds__(PSSO_CHAIN_NT, PSSO_CHAIN_MINB)
+__global__ void __launch_bounds__(PSSO_CHAIN_NT, sizeof(T) == 4 ? PSSO_CHAIN_MINB_F32 : PSSO_CHAIN_MINB)
     k_chain(const __grid_constant__ TileParams p) {
   constexpr int NTC = PSSO_CHAIN_NT;
   constexpr int NW = NTC / 32;

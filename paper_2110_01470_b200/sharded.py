@@ -240,12 +240,33 @@ class P2PExchange:
                 table.append(ptr.value)
         self.table = torch.tensor(np.array(table, dtype=np.uint64).view(np.int64), device=first.device)
 
+    @property
+    def device_loop(self) -> bool:
+        # one shard per process: whole chunks of iterations run as a graph-replayed
+        # device loop (psso_run_p2p).  Virtual shards share one stream, where one
+        # shard's loop would wait on records the next shard publishes later.
+        return self.distributed
+
     def exchange_and_apply(self, engines, cands, t: int, is_init: bool):
-        self.epoch += 1
+        # epoch 1 = initialization, t + 2 = iteration t: the same numbering the
+        # device loop derives from its iteration counter
+        self.epoch = 1 if is_init else t + 2
         for e, c, r in zip(engines, cands, self.ranks):
             e.publish_p2p(c, self.table, self.world, r, self.epoch)
         for e, buf in zip(engines, self.own):
             e.apply_p2p(t, buf, self.world, self.epoch, is_init)
+
+    def initialize(self, engines, cands):
+        for e, c in zip(engines, cands):
+            e.init_local(c)
+        self.exchange_and_apply(engines, cands, -1, True)
+
+    def run(self, engines, t0: int, niter: int):
+        from . import _lib
+
+        for e, buf, r in zip(engines, self.own, self.ranks):
+            _lib.check(self.L.psso_run_p2p(e.ctx, int(t0), int(niter), self.table.data_ptr(), buf,
+                                           self.world, r), e.ctx)
 
     def close(self):
         import ctypes
@@ -284,7 +305,9 @@ class ShardedDriver:
         return gathered
 
     def initialize(self):
-        if getattr(self.exchange, "device_loop", False):
+        if isinstance(self.exchange, P2PExchange):
+            self.exchange.initialize(self.engines, self.cands)
+        elif getattr(self.exchange, "device_loop", False):
             self.exchange.initialize(self.engines)
         else:
             for e, c in zip(self.engines, self.cands):
