@@ -116,13 +116,16 @@ int psso_run(psso_ctx* ctx, int64_t t0, int64_t niter);
 /* replaces: the loop of run_sequential (core.py:222-244), the per-particle
  * asynchronous schedule: particles updated in index order against the LIVE
  * gbest, which moves as soon as a new pbest is <= g_f (core.py:236-241).
- * Same keyed draws as psso_run; trajectory[t] = g_f after iteration t.  ONE
- * launch (k_seq): each iteration runs as speculative passes -- all remaining
- * particles computed in parallel against the current gbest, the prefix up to
- * the first gbest move (or non-finite fitness) committed, the next pass
- * starting after it -- so results are bit-identical to the serial loop.
- * Unsharded contexts, nvar <= 128 (else PSSO_E_INVALID / PSSO_E_UNSUPPORTED).
- * Call psso_init first (core.py:220).  Asynchronous. */
+ * Same keyed draws as psso_run; trajectory[t] = g_f after iteration t.  Each
+ * iteration runs as speculative passes -- all remaining particles computed in
+ * parallel against the current gbest, the prefix up to the first gbest move
+ * (or non-finite fitness) committed, the next pass starting after it -- so
+ * results are bit-identical to the serial loop.  nvar <= 128: ONE launch
+ * (k_seq, asynchronous).  Longer rows: a pass loop of device kernels over the
+ * resident swarm (search + evaluate into scratch, first-event search, commit,
+ * gbest move); the host reads 16 bytes per pass, so the call returns when the
+ * iterations are done.  Unsharded contexts (else PSSO_E_INVALID).  Call
+ * psso_init first (core.py:220). */
 int psso_run_sequential(psso_ctx* ctx, int64_t t0, int64_t niter);
 
 /* Passes k_seq ran in the last psso_run_sequential (iterations + gbest moves

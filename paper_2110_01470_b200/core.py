@@ -134,12 +134,13 @@ def run_sequential(params: SsoParams, f, seed: int, *, dtype: str = "float64",
 
     Particles are updated in index order against the live gBest, which moves
     as soon as a particle's new pBest is ``<=`` g_f (core.py:236-241); same
-    keyed draws as ``run_parallel``.  The whole loop is ONE kernel launch
-    (``psso_run_sequential``): each iteration runs as speculative passes over
-    the remaining particles, committing the prefix up to the first gBest move,
-    so the result is bit-identical to the serial loop.  ``wall_time_s`` is the
-    loop-only device time (core.py:222,245).  Rows longer than the kernel's 128
-    variables run the same passes host-driven (``_sequential_passes``).
+    keyed draws as ``run_parallel``.  Each iteration runs as speculative passes
+    over the remaining particles, committing the prefix up to the first gBest
+    move, so the result is bit-identical to the serial loop: for rows of up to
+    128 variables the whole loop is ONE kernel launch (k_seq), longer rows run
+    the same passes as a loop of device kernels over the resident swarm
+    (``psso_run_sequential`` either way).  ``wall_time_s`` is the loop-only
+    device time (core.py:222,245).
     """
     import torch
 
@@ -149,19 +150,16 @@ def run_sequential(params: SsoParams, f, seed: int, *, dtype: str = "float64",
     eng = DeviceEngine(params, f, seed, dtype=dtype, rng=rng, device=device)
     try:
         eng.initialize()
-        if params.nvar > 128:
-            trajectory, best_position, best, wall = _sequential_passes(eng, params)
-        else:
-            start = torch.cuda.Event(enable_timing=True)
-            stop = torch.cuda.Event(enable_timing=True)
-            start.record(eng.stream)
-            eng.run_sequential(0, params.niter)
-            stop.record(eng.stream)
-            eng.check()
-            wall = start.elapsed_time(stop) * 1e-3
-            trajectory = eng.traj.cpu().numpy()
-            best_position = eng.gbest.to(torch.float64).cpu().numpy()
-            best = float(eng.g_f.cpu()[0])
+        start = torch.cuda.Event(enable_timing=True)
+        stop = torch.cuda.Event(enable_timing=True)
+        start.record(eng.stream)
+        eng.run_sequential(0, params.niter)  # k_seq, or the device pass loop for nvar > 128
+        stop.record(eng.stream)
+        eng.check()
+        wall = start.elapsed_time(stop) * 1e-3
+        trajectory = eng.traj.cpu().numpy()
+        best_position = eng.gbest.to(torch.float64).cpu().numpy()
+        best = float(eng.g_f.cpu()[0])
     finally:
         eng.close()
     return RunRecord(
@@ -180,62 +178,3 @@ def run_sequential(params: SsoParams, f, seed: int, *, dtype: str = "float64",
         best_position=best_position,
         trajectory=trajectory,
     )
-
-
-def _sequential_passes(eng, params: SsoParams):
-    """run_sequential's loop (core.py:222-244) for rows longer than k_seq takes.
-
-    The same speculative passes as k_seq, driven from the host: each pass runs
-    the device search kernel over the swarm (every row against the current
-    gBest) and the device objective over rows ``[lo, N)``; the host finds the
-    first event (non-finite fitness, or a pBest ``<=`` that is also ``<=``
-    g_f), commits rows ``lo..r*`` and moves gBest.  Bit-identical to the serial
-    loop; one device round trip per pass.  Returns (trajectory, gbest, g_f,
-    wall seconds).
-    """
-    import time
-
-    import torch
-
-    from . import _lib
-
-    L = _lib.load()
-    sw = eng.to_host()
-    N = params.nsol
-    traj = np.empty(params.niter)
-    out = torch.empty(N, dtype=torch.float64, device=eng.device)
-    code = eng.cfg.fn_id
-    t_start = time.perf_counter()
-    for t in range(params.niter):
-        lo = 0
-        while lo < N:
-            eng.load(sw)                     # the committed swarm, current gbest
-            eng.search(t)                    # core.py:225,227-230 for every row
-            a = lo - lo % 4                  # 16-byte aligned first row for any nvar / dtype
-            _lib.check(L.psso_eval_rows(code, eng.cfg.dtype, params.nvar,
-                                        eng.sol[a:].data_ptr(), N - a, out[a:].data_ptr(),
-                                        eng.cfg.probe_level, eng.stream.cuda_stream))
-            eng.synchronize()
-            x = eng.sol.to(torch.float64).cpu().numpy()
-            fx = out.cpu().numpy()
-            ev = None
-            for r in range(lo, N):           # first event in serial order
-                if not np.isfinite(fx[r]) or (fx[r] <= sw.p_f[r] and fx[r] <= sw.g_f):
-                    ev = r
-                    break
-            hi = N - 1 if ev is None else ev
-            for r in range(lo, hi + 1):      # commit (core.py:231-238)
-                sw.sol[r] = x[r]
-                sw.sol_f[r] = fx[r]
-                if np.isfinite(fx[r]) and fx[r] <= sw.p_f[r]:
-                    sw.pbests[r] = x[r]
-                    sw.p_f[r] = fx[r]
-            if ev is not None:
-                if not np.isfinite(fx[ev]):
-                    raise NonFiniteFitnessError(float(fx[ev]), ev, t)  # core.py:233-234
-                sw.gbest[:] = x[ev]              # core.py:239-241
-                sw.g_f = float(fx[ev])
-            lo = N if ev is None else ev + 1
-        traj[t] = sw.g_f
-    wall = time.perf_counter() - t_start
-    return traj, sw.gbest.copy(), float(sw.g_f), wall

@@ -301,8 +301,7 @@ __global__ void __launch_bounds__(GB_THREADS) k_gbest(const __grid_constant__ Gb
 
 // Local stage 2 for sharded runs: this rank's (p_f, index, row) record.
 template <typename T>
-__global__ void __launch_bounds__(GB_THREADS) k_local_cand(const __grid_constant__ GbParams g,
-                                                           unsigned char* rec) {
+__device__ __forceinline__ void local_cand_body(const GbParams& g, unsigned char* rec) {
   __shared__ double sf[GB_THREADS / 32];
   __shared__ int64_t si[GB_THREADS / 32];
   double bf;
@@ -326,6 +325,12 @@ __global__ void __launch_bounds__(GB_THREADS) k_local_cand(const __grid_constant
     *reinterpret_cast<unsigned long long*>(rec + 16) = key;
     *reinterpret_cast<double*>(rec + 24) = v;
   }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(GB_THREADS) k_local_cand(const __grid_constant__ GbParams g,
+                                                           unsigned char* rec) {
+  local_cand_body<T>(g, rec);
 }
 
 // the run's first non-finite fitness over the gathered records: the minimum
@@ -411,11 +416,9 @@ __device__ __forceinline__ unsigned long long p2p_epoch(unsigned long long epoch
   return t_dev ? (unsigned long long)(*t_dev + 2) : epoch;
 }
 
-__global__ void __launch_bounds__(GB_THREADS) k_publish(const unsigned char* cand,
-                                                        unsigned char* const* bufs, int R, int rank,
-                                                        unsigned long long epoch_arg, int64_t rec_bytes,
-                                                        int64_t flag_bytes, const int64_t* t_dev) {
-  const unsigned long long epoch = p2p_epoch(epoch_arg, t_dev);
+__device__ __forceinline__ void publish_body(const unsigned char* cand, unsigned char* const* bufs,
+                                             int R, int rank, unsigned long long epoch,
+                                             int64_t rec_bytes, int64_t flag_bytes) {
   const uint64_t* src = reinterpret_cast<const uint64_t*>(cand);
   const int64_t words = rec_bytes / 8;
   const int slot = (int)(epoch & 1) * R + rank;  // records double-buffered by epoch parity
@@ -429,6 +432,26 @@ __global__ void __launch_bounds__(GB_THREADS) k_publish(const unsigned char* can
     for (int q = 0; q < R; ++q)
       st_release_sys_u64(reinterpret_cast<unsigned long long*>(bufs[q]) + slot, epoch);
   }
+}
+
+__global__ void __launch_bounds__(GB_THREADS) k_publish(const unsigned char* cand,
+                                                        unsigned char* const* bufs, int R, int rank,
+                                                        unsigned long long epoch_arg, int64_t rec_bytes,
+                                                        int64_t flag_bytes, const int64_t* t_dev) {
+  publish_body(cand, bufs, R, rank, p2p_epoch(epoch_arg, t_dev), rec_bytes, flag_bytes);
+}
+
+// the device loop's record + publish in one kernel: this rank's record (as
+// k_local_cand), then stored into every rank's buffer with the epoch flags
+template <typename T>
+__global__ void __launch_bounds__(GB_THREADS) k_local_cand_publish(const __grid_constant__ GbParams g,
+                                                                   unsigned char* rec,
+                                                                   unsigned char* const* bufs, int R,
+                                                                   int rank, int64_t rec_bytes,
+                                                                   int64_t flag_bytes) {
+  local_cand_body<T>(g, rec);
+  __syncthreads();  // the record (global, written by this block) is complete
+  publish_body(rec, bufs, R, rank, p2p_epoch(0, g.t_dev), rec_bytes, flag_bytes);
 }
 
 template <typename T>
@@ -530,6 +553,84 @@ __global__ void k_inv_sqrt(double* aux, int D) {  // 1.0 / np.sqrt(np.arange(1, 
 __global__ void k_set(int64_t* p, int64_t v) { *p = v; }
 __global__ void k_set_u64(unsigned long long* p, unsigned long long v) { *p = v; }
 
+// ---- the sequential schedule for rows beyond the chain mapping (nvar > 128):
+// the same speculative passes as k_seq (psso_seq.cuh), as a pass loop of
+// kernels over the HBM-resident swarm.  ctl = [lo, first event, failed].
+// First event in [lo, N): a non-finite fitness (core.py:233) or a pBest `<=`
+// that is also `<=` g_f (core.py:236-241).  One CTA; lowest index wins.
+__global__ void __launch_bounds__(1024) k_seq_event(const double* fn, const double* p_f,
+                                                    const double* g_f, int64_t* ctl, int64_t N) {
+  __shared__ int64_t red[32];
+  const int64_t lo = ctl[0];
+  const double gf = *g_f;
+  int64_t ev = INT64_MAX;
+  for (int64_t r = lo + threadIdx.x; r < N; r += blockDim.x) {
+    const double f = fn[r];
+    if (!isfinite(f) || (f <= p_f[r] && f <= gf)) { ev = r; break; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ev = min(ev, (int64_t)__shfl_xor_sync(0xffffffffu, ev, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ev;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    ev = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : INT64_MAX;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ev = min(ev, (int64_t)__shfl_xor_sync(0xffffffffu, ev, o));
+    if (threadIdx.x == 0) ctl[1] = ev == INT64_MAX ? N : ev;
+  }
+}
+
+// commit rows lo..min(ev, N-1): X always (core.py:231), pBest on `<=` (:236-238)
+template <typename T>
+__global__ void k_seq_commit(T* X, T* P, const T* Xn, const double* fn, double* p_f, double* sol_f,
+                             const int64_t* ctl, int64_t N, int D) {
+  const int64_t lo = ctl[0], hi = min(ctl[1], N - 1);
+  for (int64_t r = lo + blockIdx.x; r <= hi; r += gridDim.x) {
+    const double f = fn[r];
+    const bool imp = isfinite(f) && f <= p_f[r];
+    const T* src = Xn + r * (int64_t)D;
+    for (int j = threadIdx.x; j < D; j += blockDim.x) {
+      const T v = src[j];
+      X[r * (int64_t)D + j] = v;
+      if (imp) P[r * (int64_t)D + j] = v;
+    }
+    __syncthreads();  // every thread read p_f[r] before it moves
+    if (threadIdx.x == 0) {
+      if (sol_f) sol_f[r] = f;
+      if (imp) p_f[r] = f;
+    }
+  }
+}
+
+// the event: gbest <- pbests[r*] (core.py:239-241) or the non-finite stop;
+// next pass from r* + 1; trajectory[t] once the iteration is complete (:242)
+template <typename T>
+__global__ void k_seq_move(T* gbest, const T* Xn, const double* fn, double* g_f, int64_t* g_idx,
+                           unsigned long long* bad, double* traj, int64_t t, int64_t* ctl,
+                           int64_t* passes, int64_t N, int D) {
+  __shared__ int stop;
+  const int64_t ev = ctl[1];
+  if (threadIdx.x == 0) stop = ev < N && !isfinite(fn[ev]);
+  __syncthreads();
+  if (ev < N && !stop)
+    for (int j = threadIdx.x; j < D; j += blockDim.x) gbest[j] = Xn[ev * (int64_t)D + j];
+  if (threadIdx.x == 0) {
+    if (passes) *passes += 1;
+    if (stop) {
+      if (bad) atomicMin(bad, ((unsigned long long)(t + 1) << 40) | (unsigned long long)ev);
+      ctl[2] = 1;
+      ctl[0] = N;
+    } else {
+      if (ev < N) {
+        *g_f = fn[ev];
+        if (g_idx) *g_idx = ev;
+      }
+      ctl[0] = ev < N ? ev + 1 : N;
+      if (ctl[0] >= N && traj) traj[t] = *g_f;
+    }
+  }
+}
+
 }  // namespace
 
 // ------------------------------------------------------------- context ----
@@ -590,6 +691,8 @@ struct psso_ctx {
   double* seq_pfn;       // rows scratch
   uint64_t* seq_seed;
   int64_t* seq_passes;
+  int64_t* seq_ctl;      // long-row sequential passes: [lo, event, failed, -]
+  int64_t* seq_ctl_host; // pinned copy
   // sharded iteration over a library-owned NCCL communicator (psso_attach_nccl)
   void* comm;            // ncclComm_t, borrowed from a psso_comm
   int32_t nranks, rank;
@@ -1180,6 +1283,8 @@ void psso_destroy(psso_ctx* c) {
   cudaFree(c->seq_pfn);
   cudaFree(c->seq_seed);
   cudaFree(c->seq_passes);
+  cudaFree(c->seq_ctl);
+  if (c->seq_ctl_host) cudaFreeHost(c->seq_ctl_host);
   delete c;
 }
 
@@ -1390,6 +1495,80 @@ static cudaError_t launch_seq(psso_ctx* c, int M, SeqParams q, int64_t B, cudaSt
 
 // run_sequential (core.py:213-258): one k_seq launch for the whole loop
 // (speculative passes with rollback, psso_seq.cuh).
+// run_sequential (core.py:222-244) for rows the chain mapping does not take
+// (nvar > 128): per iteration, speculative passes until the swarm's end --
+// every remaining row searched and evaluated against the current gbest into
+// scratch (X -> Xn copy, then the tile kernel's search + evaluate on Xn; the
+// non-finite flag is not touched speculatively), the first event found,
+// rows up to it committed, gbest moved -- all on the device; the host reads
+// back 16 bytes per pass (where the next pass starts, whether the run failed).
+// Bit-identical to the serial loop for the same reason as k_seq.
+static int run_sequential_rows(psso_ctx* c, int64_t t0, int64_t niter) {
+  const psso_config* cfg = &c->cfg;
+  const int64_t N = cfg->nsol, D = cfg->nvar;
+  const int es = cfg->dtype == PSSO_F64 ? 8 : 4;
+  if (!c->seq_xn) {
+    CK(c, cudaMalloc(&c->seq_xn, (size_t)N * D * es));
+    CK(c, cudaMalloc(&c->seq_fn, (size_t)N * sizeof(double)));
+    CK(c, cudaMalloc(&c->seq_passes, sizeof(int64_t)));
+    CK(c, cudaMemset(c->seq_passes, 0, sizeof(int64_t)));
+  }
+  if (!c->seq_ctl) {
+    CK(c, cudaMalloc(&c->seq_ctl, 4 * sizeof(int64_t)));
+    CK(c, cudaMallocHost(&c->seq_ctl_host, 4 * sizeof(int64_t)));
+  }
+  {  // a run that already failed stays stopped (like the kernels' early exit)
+    unsigned long long key = ~0ull;
+    CK(c, cudaMemcpyAsync(&key, c->bad, sizeof key, cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    if (key != ~0ull) return PSSO_OK;
+  }
+  CK(c, cudaMemsetAsync(c->seq_passes, 0, sizeof(int64_t), c->stream));
+  CK(c, cudaMemsetAsync(c->seq_ctl, 0, 4 * sizeof(int64_t), c->stream));
+  const int commit_grid = (int)std::min<int64_t>(N, 8 * c->num_sms);
+  unsigned char* X = (unsigned char*)c->buf.sol;
+  unsigned char* Xn = (unsigned char*)c->seq_xn;
+  for (int64_t t = t0; t < t0 + niter; ++t) {
+    int64_t lo = 0;
+    k_set<<<1, 1, 0, c->stream>>>(c->seq_ctl, 0);
+    c->launches++;
+    while (lo < N) {
+      const int64_t a = lo - lo % 4;  // 16-byte aligned first row for any nvar / dtype
+      CK(c, cudaMemcpyAsync(Xn + (size_t)a * D * es, X + (size_t)a * D * es, (size_t)(N - a) * D * es,
+                            cudaMemcpyDeviceToDevice, c->stream));
+      TileParams p = tile_params(c, M_SEARCH | M_EVAL | M_SOLF, t, nullptr, false);
+      p.X = Xn + (size_t)a * D * es;
+      p.P = (unsigned char*)c->buf.pbests + (size_t)a * D * es;
+      p.p_f = c->buf.p_f + a;
+      p.sol_f = c->seq_fn + a;
+      p.rows = N - a;
+      p.row_lo = a;
+      p.bad = nullptr;  // speculative: a non-finite row counts only if it is the first event
+      if (int rc = launch_tile(c, p)) return rc;
+      k_seq_event<<<1, 1024, 0, c->stream>>>(c->seq_fn, c->buf.p_f, c->buf.g_f, c->seq_ctl, N);
+      if (cfg->dtype == PSSO_F64) {
+        k_seq_commit<double><<<commit_grid, 256, 0, c->stream>>>((double*)c->buf.sol, (double*)c->buf.pbests,
+            (const double*)c->seq_xn, c->seq_fn, c->buf.p_f, c->buf.sol_f, c->seq_ctl, N, (int)D);
+        k_seq_move<double><<<1, 256, 0, c->stream>>>((double*)c->buf.gbest, (const double*)c->seq_xn,
+            c->seq_fn, c->buf.g_f, c->g_idx, c->bad, c->buf.traj, t, c->seq_ctl, c->seq_passes, N, (int)D);
+      } else {
+        k_seq_commit<float><<<commit_grid, 256, 0, c->stream>>>((float*)c->buf.sol, (float*)c->buf.pbests,
+            (const float*)c->seq_xn, c->seq_fn, c->buf.p_f, c->buf.sol_f, c->seq_ctl, N, (int)D);
+        k_seq_move<float><<<1, 256, 0, c->stream>>>((float*)c->buf.gbest, (const float*)c->seq_xn,
+            c->seq_fn, c->buf.g_f, c->g_idx, c->bad, c->buf.traj, t, c->seq_ctl, c->seq_passes, N, (int)D);
+      }
+      c->launches += 3;
+      CK(c, cudaGetLastError());
+      CK(c, cudaMemcpyAsync(c->seq_ctl_host, c->seq_ctl, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                            c->stream));
+      CK(c, cudaStreamSynchronize(c->stream));
+      if (c->seq_ctl_host[2]) return PSSO_OK;  // non-finite: reported by psso_check
+      lo = c->seq_ctl_host[0];
+    }
+  }
+  return PSSO_OK;
+}
+
 int psso_run_sequential(psso_ctx* c, int64_t t0, int64_t niter) {
   DEV_GUARD(c);
   if (int rc = need_bound(c)) return rc;
@@ -1397,8 +1576,7 @@ int psso_run_sequential(psso_ctx* c, int64_t t0, int64_t niter) {
   const psso_config* cfg = &c->cfg;
   if (cfg->row_lo != 0 || cfg->row_hi != cfg->nsol)
     return fail(c, PSSO_E_INVALID, "the sequential schedule runs unsharded swarms only");
-  if (!c->chain)
-    return fail(c, PSSO_E_UNSUPPORTED, "the sequential schedule supports nvar <= 128 (chain-mapped rows)");
+  if (!c->chain) return run_sequential_rows(c, t0, niter);
   const int64_t rows = cfg->nsol, D = cfg->nvar;
   const int M = D <= 32 ? 4 : D <= 64 ? 8 : 16;
   const int es = cfg->dtype == PSSO_F64 ? 8 : 4;
@@ -1732,10 +1910,14 @@ int psso_apply_p2p(psso_ctx* c, int64_t t, const void* my_buf, int32_t nranks, u
 static int p2p_step_dev(psso_ctx* c, const void* peer_bufs, const void* my_buf, int32_t nranks,
                         int32_t rank) {
   if (int rc = launch_fused(c, 0, c->t_dev)) return rc;
-  if (int rc = local_cand(c, c->cand, c->fused_grid)) return rc;
   const int64_t rb = psso_candidate_bytes(&c->cfg), fb = (int64_t)align16((size_t)nranks * 16);
-  k_publish<<<1, GB_THREADS, 0, c->stream>>>(c->cand, (unsigned char* const*)peer_bufs, nranks, rank, 0,
-                                             rb, fb, c->t_dev);
+  GbParams gl = gb_params(c, 0, c->t_dev, 0, c->fused_grid);
+  if (c->cfg.dtype == PSSO_F64)
+    k_local_cand_publish<double><<<1, GB_THREADS, 0, c->stream>>>(gl, c->cand, (unsigned char* const*)peer_bufs,
+                                                                  nranks, rank, rb, fb);
+  else
+    k_local_cand_publish<float><<<1, GB_THREADS, 0, c->stream>>>(gl, c->cand, (unsigned char* const*)peer_bufs,
+                                                                 nranks, rank, rb, fb);
   GbParams g = gb_params(c, 0, c->t_dev, 0, 0);
   if (c->cfg.dtype == PSSO_F64)
     k_apply_p2p<double><<<1, GB_THREADS, 0, c->stream>>>(g, (const unsigned char*)my_buf, nranks, 0, rb, fb);
@@ -1763,7 +1945,7 @@ int psso_run_p2p(psso_ctx* c, int64_t t0, int64_t niter, void* const* peer_bufs,
   int64_t done = 0;
   const bool graph = c->stream != nullptr && !c->profiling;
   if (graph && niter >= GRAPH_CHUNK) {
-    if (!c->pgraph) {  // GRAPH_CHUNK x (fused kernel, record, publish, apply)
+    if (!c->pgraph) {  // GRAPH_CHUNK x (fused kernel, record + publish, apply)
       cudaGraph_t gr;
       CK(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
       const int64_t saved = c->launches;
@@ -1783,7 +1965,7 @@ int psso_run_p2p(psso_ctx* c, int64_t t0, int64_t niter, void* const* peer_bufs,
     }
     for (; done + GRAPH_CHUNK <= niter; done += GRAPH_CHUNK) {
       CK(c, cudaGraphLaunch(c->pgraph, c->stream));
-      c->launches += 4 * GRAPH_CHUNK;
+      c->launches += 3 * GRAPH_CHUNK;
     }
   }
   for (; done < niter; ++done)  // same kernels, launched directly

@@ -159,22 +159,52 @@ def test_sequential_nonfinite_names_first_particle():
         pytest.fail("oracle replay never hit the probe")
 
 
-def test_sequential_kernel_rejects_long_rows():
-    """psso_run_sequential (k_seq) takes nvar <= 128; run_sequential covers the rest host-driven."""
-    fn = psso.make_function("f1", 200)
-    p = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=-5.12, var_max=5.12, nsol=10, nvar=200,
-                       niter=3)
-    eng = DeviceEngine(p, fn, 0)
+def test_sequential_long_rows_run_on_the_device_state_resident():
+    """nvar > 128: psso_run_sequential's device pass loop, stepwise == the oracle's serial
+    loop iteration by iteration (state, gBest index, pass count), no host state round trips."""
+    fn = psso.make_function("f5", 300)
+    p = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=fn.var_min, var_max=fn.var_max, nsol=70,
+                       nvar=300, niter=6)
+    eng = DeviceEngine(p, fn, 4, keep_sol_f=True)
+    o = O.Oracle.from_params(p, "f5", 4)
+    osw = o.initialize()
     try:
         eng.initialize()
-        with pytest.raises(psso._lib.PssoError, match="nvar <= 128"):
-            eng.run_sequential(0, 3)
+        for t in range(p.niter):
+            eng.run_sequential(t, 1)
+            eng.check()
+            o.step_sequential(osw, t)
+            sw = eng.to_host()
+            assert np.array_equal(sw.sol, osw.sol) and np.array_equal(sw.pbests, osw.pbests), t
+            assert np.array_equal(sw.gbest, osw.gbest), t
+            assert np.allclose(sw.p_f, osw.p_f, rtol=1e-12, atol=0), t
+            gf, gi = eng.result()  # the last particle that moved gbest holds it as its pBest
+            assert np.array_equal(osw.pbests[gi], osw.gbest), t
+            assert eng.sequential_passes >= 1
     finally:
         eng.close()
 
 
+def test_sequential_long_rows_nonfinite_names_particle():
+    level = float(O.init_positions(0, 40, 200, -1.0, 1.0)[:, 0].max())
+    fn = psso.probe_function(200, level=level, bounds=(-1.0, 1.0))
+    p = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=-1, var_max=1, nsol=40, nvar=200, niter=100)
+    with pytest.raises(psso.NonFiniteFitnessError) as ei:
+        psso.run_sequential(p, fn, seed=0)
+    o = O.Oracle("f1", 40, 200, 0.3, 0.6, 0.8, -1.0, 1.0, 0)
+    sw = o.initialize()
+    for t in range(p.niter):
+        o.step_sequential(sw, t)
+        bad = np.nonzero(sw.sol[:, 0] > level)[0]
+        if bad.size:
+            assert (t, int(bad[0])) == (ei.value.iteration, ei.value.particle)
+            return
+    pytest.fail("oracle replay never hit the probe")
+
+
 @pytest.mark.parametrize("fid,nsol,nvar,niter", [("f1", 60, 200, 12), ("f5", 40, 300, 10),
-                                                  ("f4", 30, 512, 8), ("f7", 25, 129, 10)])
+                                                  ("f4", 30, 512, 8), ("f7", 25, 129, 10),
+                                                  ("f6", 300, 4096, 4), ("f3", 50, 130, 6)])
 def test_sequential_long_rows_against_oracle(fid, nsol, nvar, niter):
     fn = _fn(fid, nvar)
     p = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=fn.var_min, var_max=fn.var_max,
