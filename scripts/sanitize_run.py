@@ -50,3 +50,29 @@ for fid, n, d, it in (("f1", 100, 30, 20), ("f7", 70, 20, 10), ("f5", 300, 128, 
     rec = psso.run_sequential(psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=fn.var_min,
                                              var_max=fn.var_max, nsol=n, nvar=d, niter=it), fn, 2)
     print("ok sequential", fid, n, d, flush=True)
+for fid, n, d, it in (("f5", 40, 300, 3), ("f6", 20, 4096, 2)):  # long-row sequential pass loop
+    fn = psso.make_function(fid, d)
+    rec = psso.run_sequential(psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=fn.var_min,
+                                             var_max=fn.var_max, nsol=n, nvar=d, niter=it), fn, 2)
+    print("ok sequential (device pass loop)", fid, n, d, flush=True)
+for fid, n, d, dt in (("f5", 5000, 128, "float32"), ("f6", 40, 4096, "float64")):  # Philox mode
+    fn = psso.make_function(fid, d)
+    rec = psso.run_parallel(psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=fn.var_min,
+                                           var_max=fn.var_max, nsol=n, nvar=d, niter=3), fn, 2,
+                            dtype=dt, rng="philox")
+    print("ok philox", fid, dt, flush=True)
+# library NCCL communicator + graph-replayed sharded loop, and the P2P device loop (world size 1)
+import torch.distributed as dist  # noqa: E402
+
+os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=os.environ.get("SAN_PORT", "29561"), RANK="0",
+                  WORLD_SIZE="1")
+dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+from paper_2110_01470_b200.sharded import run_parallel_distributed  # noqa: E402
+
+fn = psso.make_function("f4", 64)
+p = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=fn.var_min, var_max=fn.var_max, nsol=3000,
+                   nvar=64, niter=20)
+for ex in ("nccl", "p2p"):
+    rec = run_parallel_distributed(p, fn, 2, exchange=ex)
+    print("ok distributed", ex, flush=True)
+dist.destroy_process_group()
