@@ -769,6 +769,16 @@ TileParams tile_params(psso_ctx* c, int mode, int64_t t, const int64_t* t_dev, b
   p.div_D = make_div((uint32_t)c->cfg.nvar);
   p.seed = c->cfg.seed;
   p.Kw = c->Kw; p.Kp = c->Kp; p.Kg = c->Kg;
+  {  // the same thresholds on the unshifted hash (K < 2^53 fits after << 11)
+    const uint64_t K[3] = {c->Kw, c->Kp, c->Kg};
+    uint64_t* K11[3] = {&p.Kw11, &p.Kp11, &p.Kg11};
+    p.Kon = 0;
+    for (int b = 0; b < 3; ++b) {
+      const bool on = K[b] < (1ull << 53);
+      *K11[b] = on ? K[b] << 11 : ~0ull;
+      p.Kon |= on ? (1 << b) : 0;
+    }
+  }
   p.Kw32 = c->Kw32; p.Kp32 = c->Kp32; p.Kg32 = c->Kg32;
   p.var_min = c->cfg.var_min;
   p.span = c->cfg.var_max - c->cfg.var_min;
@@ -1007,6 +1017,22 @@ cudaError_t launch_swarm(const SwarmPlan& pl, int64_t B, void** args, cudaStream
 // (psso_solve, psso_solve_batch): the device's default memory pool keeps
 // freed blocks cached (release threshold = max), so repeated calls do not
 // pay for mapping and unmapping gigabytes of HBM.
+// One persistent stream per host thread (and device) for the one-shot entry
+// points: blocks freed on a stream are reusable by the next call's
+// allocations on the SAME stream without any cross-stream dependency, so
+// repeated calls never map fresh HBM (with a new stream per call every other
+// 16 GiB call paid ~0.7 s of mapping).
+cudaError_t solve_stream(cudaStream_t* s) {
+  thread_local cudaStream_t st[64] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  if (!st[dev] && (e = cudaStreamCreateWithFlags(&st[dev], cudaStreamNonBlocking)) != cudaSuccess) return e;
+  *s = st[dev];
+  return cudaSuccess;
+}
+
 cudaError_t pool_alloc(void** p, size_t bytes, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
@@ -2160,9 +2186,9 @@ int psso_solve(const psso_config* cfg, int64_t niter, double* traj, void* best_p
     mark("freeasync");
     if (e0) cudaEventDestroy(e0);
     if (e1) cudaEventDestroy(e1);
-    if (s) { cudaStreamSynchronize(s); mark("streamsync"); cudaStreamDestroy(s); }
+    if (s) { cudaStreamSynchronize(s); mark("streamsync"); }
   };
-  if ((e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) != cudaSuccess ||
+  if ((e = solve_stream(&s)) != cudaSuccess ||
       (e = cudaEventCreate(&e0)) != cudaSuccess || (e = cudaEventCreate(&e1)) != cudaSuccess ||
       (e = pool_alloc(&b.sol, N * D * es, s)) != cudaSuccess ||
       (e = pool_alloc(&b.pbests, N * D * es, s)) != cudaSuccess ||
@@ -2245,10 +2271,10 @@ static int solve_batch(const psso_config* cfg, const uint64_t* seeds, int32_t ns
       if (b->p) cudaFreeAsync(b->p, s);
     if (e0) cudaEventDestroy(e0);
     if (e1) cudaEventDestroy(e1);
-    if (s) { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
+    if (s) cudaStreamSynchronize(s);
     psso_destroy(c);
   };
-  if ((e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) != cudaSuccess ||
+  if ((e = solve_stream(&s)) != cudaSuccess ||
       (e = cudaEventCreate(&e0)) != cudaSuccess || (e = cudaEventCreate(&e1)) != cudaSuccess ||
       (e = pool_alloc(&X.p, B * N * D * es, s)) != cudaSuccess ||
       (e = pool_alloc(&P.p, B * N * D * es, s)) != cudaSuccess ||
