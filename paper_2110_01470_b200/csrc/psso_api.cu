@@ -769,15 +769,6 @@ TileParams tile_params(psso_ctx* c, int mode, int64_t t, const int64_t* t_dev, b
   p.div_D = make_div((uint32_t)c->cfg.nvar);
   p.seed = c->cfg.seed;
   p.Kw = c->Kw; p.Kp = c->Kp; p.Kg = c->Kg;
-  {  // the same thresholds on the unshifted hash (K < 2^53 fits after << 11)
-    const uint64_t K[3] = {c->Kw, c->Kp, c->Kg};
-    uint64_t* K11[3] = {&p.Kw11, &p.Kp11, &p.Kg11};
-    p.Kon = 0;
-    for (int b = 0; b < 3; ++b) {
-      const bool on = K[b] < (1ull << 53);
-      *K11[b] = on ? K[b] << 11 : ~0ull;
-      p.Kon |= on ? (1 << b) : 0;
-    }
   }
   p.Kw32 = c->Kw32; p.Kp32 = c->Kp32; p.Kg32 = c->Kg32;
   p.var_min = c->cfg.var_min;

@@ -92,9 +92,6 @@ struct TileParams {
   int32_t fn_pad;
   uint64_t seed;
   uint64_t Kw, Kp, Kg;         // reference mode: branch k = h >> 11 compared < K
-  uint64_t Kw11, Kp11, Kg11;   // the same tests on h itself: h >> 11 >= K <=> h >= K << 11;
-  int32_t Kon;                 // bit b: threshold b < 2^53 (K << 11 fits; else never taken)
-  int32_t pad_k;
   uint64_t Kw32, Kp32, Kg32;   // philox mode: 32-bit word compared < K32
   double var_min, span;
   double span53;               // span * 2^-53 (fresh = var_min + k * span53, exact rescale)
@@ -584,18 +581,6 @@ __device__ void tile_fitness(const TileParams& p, const T* xsrc, int SX, T* buf,
 // lane needs it, so predication is free), and the cumulative thresholds turn
 // the select chain into three monotone compares:
 //   k >= Kw -> pbest, k >= Kp -> gbest, k >= Kg -> fresh   (else keep x)
-// The four-way select (core.py:160-173) on the full 64-bit branch hash h:
-// (h >> 11) >= K <=> h >= K << 11, so the shift is folded into the
-// thresholds; a threshold of 1.0 (K = 2^53, never taken) is off in p.Kon.
-template <typename T>
-__device__ __forceinline__ T ref_select(const TileParams& p, uint64_t h, T x, T pb, T gv, T fresh) {
-  T a = x;
-  a = (h >= p.Kw11 && (p.Kon & 1)) ? pb : a;
-  a = (h >= p.Kp11 && (p.Kon & 2)) ? gv : a;
-  a = (h >= p.Kg11 && (p.Kon & 4)) ? fresh : a;
-  return a;
-}
-
 // The four-way select (core.py:160-173) from one half of a Philox pair:
 // branch word w[h] against the 32-bit thresholds, fresh = var_min + span * w[2+h] 2^-32.
 // fp32 (benchmark mode has no bitwise contract): the fresh draw in fp32,
@@ -1230,9 +1215,12 @@ __device__ __forceinline__ bool chain_step(const TileParams& p, const ChainEnv& 
       }
       if constexpr (RNG == 0) {
         const uint64_t gx = xg[j];
-        const uint64_t hb = mix64_tail<(M <= 8 || sizeof(T) == 8)>(xb ^ gx);
+        const uint64_t kb = mix64_tail<(M <= 8 || sizeof(T) == 8)>(xb ^ gx) >> 11;
         const double fresh = __dadd_rn(p.var_min, fresh_offset<(M <= 8 || sizeof(T) == 8)>(xf ^ gx, p.span64));
-        v = ref_select<T>(p, hb, x[m], pv[m], gb[j], (T)fresh);
+        v = x[m];
+        v = kb >= p.Kw ? pv[m] : v;
+        v = kb >= p.Kp ? gb[j] : v;
+        v = kb >= p.Kg ? (T)fresh : v;
       } else {
         v = philox_select<T>(p, w, m & 1, x[m], pv[m], gb[j]);
       }
@@ -1674,9 +1662,12 @@ __global__ void __launch_bounds__(256, 2) k_rows(const __grid_constant__ TilePar
         for (int m = 0; m < M; ++m) {
           const int j = jb + 8 * m;
           const uint64_t gx = xs30(g0 + GAMMA * (uint64_t)(8 * m));
-          const uint64_t hb = mix64_tail<(sizeof(T) == 8)>(xb ^ gx);
+          const uint64_t kb = mix64_tail<(sizeof(T) == 8)>(xb ^ gx) >> 11;
           const double fresh = __dadd_rn(p.var_min, fresh_offset<(sizeof(T) == 8)>(xf ^ gx, p.span64));
-          const T v = ref_select<T>(p, hb, x[m], pv[m], gbl[j], (T)fresh);
+          T v = x[m];
+          v = kb >= p.Kw ? pv[m] : v;
+          v = kb >= p.Kp ? gbl[j] : v;
+          v = kb >= p.Kg ? (T)fresh : v;
           x[m] = v;
           stg_stream<T, 1>(xr + j, VecT<T, 1>{{v}});
           accumulate(m, v);
