@@ -769,7 +769,6 @@ TileParams tile_params(psso_ctx* c, int mode, int64_t t, const int64_t* t_dev, b
   p.div_D = make_div((uint32_t)c->cfg.nvar);
   p.seed = c->cfg.seed;
   p.Kw = c->Kw; p.Kp = c->Kp; p.Kg = c->Kg;
-  }
   p.Kw32 = c->Kw32; p.Kp32 = c->Kp32; p.Kg32 = c->Kg32;
   p.var_min = c->cfg.var_min;
   p.span = c->cfg.var_max - c->cfg.var_min;
@@ -1004,10 +1003,6 @@ cudaError_t launch_swarm(const SwarmPlan& pl, int64_t B, void** args, cudaStream
   return cudaLaunchKernel(pl.fn, dim3(1, (unsigned)B), dim3(PSSO_SWARM_NT), args, pl.smem, s);
 }
 
-// Stream-ordered allocations for the one-shot host-buffer entry points
-// (psso_solve, psso_solve_batch): the device's default memory pool keeps
-// freed blocks cached (release threshold = max), so repeated calls do not
-// pay for mapping and unmapping gigabytes of HBM.
 // One persistent stream per host thread (and device) for the one-shot entry
 // points: blocks freed on a stream are reusable by the next call's
 // allocations on the SAME stream without any cross-stream dependency, so
@@ -1024,6 +1019,10 @@ cudaError_t solve_stream(cudaStream_t* s) {
   return cudaSuccess;
 }
 
+// Stream-ordered allocations for the one-shot host-buffer entry points
+// (psso_solve, psso_solve_batch): the device's default memory pool keeps
+// freed blocks cached (release threshold = max), so repeated calls do not
+// pay for mapping and unmapping gigabytes of HBM.
 cudaError_t pool_alloc(void** p, size_t bytes, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
