@@ -437,7 +437,9 @@ def run_ours(args, wl):
                          f"per GPU vs 126 MB L2",
                    "parallelism": f"particle shards x{ws}" + (exch if sharded else "")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": _traffic(wl, kname), "peak_source": peak_src,
+                     "frac": achieved / peak,
+                     "traffic": _traffic(wl + ("_philox" if args.rng == "philox" else ""), kname),
+                     "peak_source": peak_src,
                      "kernel": kname, "kernel_ms_per_iteration": kern_ms,
                      "alg_bytes_per_launch": alg_bytes, "alg_bytes_per_pvu": 3 * es,
                      "rho": rho, "bytes_per_pvu_with_rho": bpv_rho,

@@ -1551,8 +1551,15 @@ __host__ __device__ constexpr bool rows_fn() {
   return FN == 0 || FN == 1 || FN == 2 || FN == 5 || FN == 6 || FN == 9;
 }
 
+// PSSO_ROWS_JIT: pBest values read from the prefetch buffer just in time
+// (not held in 32 registers), the next row's prefetch issued after the draw,
+// gbest read through L1 instead of staged in shared memory -- 85 registers and
+// ~67 KB of shared memory per CTA, so 3 CTAs per SM.
+#ifndef PSSO_ROWS_JIT
+#define PSSO_ROWS_JIT 0
+#endif
 template <typename T, int FN, int RNG, int W>
-__global__ void __launch_bounds__(256, 2) k_rows(const __grid_constant__ TileParams p) {
+__global__ void __launch_bounds__(256, PSSO_ROWS_JIT ? 3 : 2) k_rows(const __grid_constant__ TileParams p) {
   using N = Num<T>;
   constexpr int NW = 8, RPC = NW / W, M = 16, D = 512 * W, NL = 4 * W;
   constexpr int RS = chain_row_stride<T, M>();
@@ -1577,12 +1584,13 @@ __global__ void __launch_bounds__(256, 2) k_rows(const __grid_constant__ TilePar
     rootb = root64(p.seed, STREAM_BRANCH, (uint64_t)t);
     rootf = root64(p.seed, STREAM_FRESH, (uint64_t)t);
   }
-  {  // gbest padded by 8 elements per leaf: the segments' reads hit disjoint banks
+  if constexpr (!PSSO_ROWS_JIT) {  // gbest padded by 8 elements per leaf: the segments' reads hit disjoint banks
     const T* g = reinterpret_cast<const T*>(p.gbest);
     for (int j = tid; j < D; j += 256) gb[j + ((j >> 7) << 3)] = g[j];
   }
   const int jb = 512 * sw + 128 * s + k;  // this lane's first element; j = jb + 8m
-  const T* gbl = gb + 8 * (4 * sw + s);   // gbest of this lane's leaf: gbl[j]
+  const T* gbl = PSSO_ROWS_JIT ? reinterpret_cast<const T*>(p.gbest)  // gbest of this lane's leaf: gbl[j]
+                               : gb + 8 * (4 * sw + s);
   const uint64_t g0 = GAMMA * (uint64_t)(jb + 1);
 
   const int64_t rows = p.rows;
@@ -1628,19 +1636,25 @@ __global__ void __launch_bounds__(256, 2) k_rows(const __grid_constant__ TilePar
     T x[M];
     const double pf_row = rv ? p.p_f[r] : 0.0;  // needed after barrier A
     if (rv) {
-      T pv[M];
+      T pv[PSSO_ROWS_JIT ? 1 : M];
       mbar_wait(wbar, wphase);
       wphase ^= 1;
       const T* xs = reinterpret_cast<const T*>(wbuf + s * RS);
       const T* ps = reinterpret_cast<const T*>(wbuf + 4 * RS + s * RS);
+      auto pbest = [&](int m) -> T { return PSSO_ROWS_JIT ? ps[k + 8 * m] : pv[PSSO_ROWS_JIT ? 0 : m]; };
+      if constexpr (!PSSO_ROWS_JIT) {
 #pragma unroll
-      for (int m = 0; m < M; ++m) {
-        x[m] = xs[k + 8 * m];
-        pv[m] = ps[k + 8 * m];
+        for (int m = 0; m < M; ++m) {
+          x[m] = xs[k + 8 * m];
+          pv[PSSO_ROWS_JIT ? 0 : m] = ps[k + 8 * m];
+        }
+        __syncwarp();
+        fence_proxy_async();
+        prefetch(r + rstride);
+      } else {
+#pragma unroll
+        for (int m = 0; m < M; ++m) x[m] = xs[k + 8 * m];
       }
-      __syncwarp();
-      fence_proxy_async();
-      prefetch(r + rstride);
 
       // ---- positions (core.py:138-173; see k_chain), each followed at once
       // by its objective terms and the in-order chain adds of leaf 4sw+s
@@ -1665,7 +1679,7 @@ __global__ void __launch_bounds__(256, 2) k_rows(const __grid_constant__ TilePar
           const uint64_t kb = mix64_tail<(sizeof(T) == 8)>(xb ^ gx) >> 11;
           const double fresh = __dadd_rn(p.var_min, fresh_offset<(sizeof(T) == 8)>(xf ^ gx, p.span64));
           T v = x[m];
-          v = kb >= p.Kw ? pv[m] : v;
+          v = kb >= p.Kw ? pbest(m) : v;
           v = kb >= p.Kp ? gbl[j] : v;
           v = kb >= p.Kg ? (T)fresh : v;
           x[m] = v;
@@ -1680,10 +1694,15 @@ __global__ void __launch_bounds__(256, 2) k_rows(const __grid_constant__ TilePar
           if ((m & 1) == 0)
             w = philox4x32_10(philox_pair(j), (uint32_t)gi, (uint32_t)(gi >> 32), (uint32_t)t,
                               (uint32_t)p.seed, (uint32_t)(p.seed >> 32));
-          x[m] = philox_select<T>(p, w, m & 1, x[m], pv[m], gbl[j]);
+          x[m] = philox_select<T>(p, w, m & 1, x[m], pbest(m), gbl[j]);
           stg_stream<T, 1>(xr + j, VecT<T, 1>{{x[m]}});
           accumulate(m, x[m]);
         }
+      }
+      if constexpr (PSSO_ROWS_JIT) {  // this row's slice is consumed: refill with the next row's
+        __syncwarp();
+        fence_proxy_async();
+        prefetch(r + rstride);
       }
 
 #pragma unroll
