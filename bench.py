@@ -86,7 +86,7 @@ def _peaks():
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
 
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+    Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
@@ -105,8 +105,22 @@ class ClockSampler:
             self.proc = None
 
     def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+        import datetime
+
+        for line in self.proc.stdout:  # (nvidia-smi's own sample time, the sample)
+            ts, _, rest = line.strip().partition(",")
+            try:
+                when = datetime.datetime.strptime(ts.strip(), "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                when = None
+            self.lines.append((when, rest))
+
+    def mark(self, begin: bool):
+        """Bracket the timed region (host wall clock, after the device syncs)."""
+        if begin:
+            self.t0 = time.time()
+        else:
+            self.t1 = time.time()
 
     def stop(self):
         if self.proc is None:
@@ -119,7 +133,13 @@ class ClockSampler:
         self.thread.join(timeout=2)
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        t0, t1 = getattr(self, "t0", None), getattr(self, "t1", None)
+        inside = [ln for ts, ln in self.lines
+                  if ts is not None and t0 is not None and t1 is not None and t0 <= ts <= t1]
+        # samples taken during the timed region; a region shorter than the sampling
+        # period keeps the samples of the whole sampling window (stated in "window")
+        window = "timed region" if inside else "timed region + 0.3 s lead-in + kernel-timing pass"
+        for ln in inside or [ln for _, ln in self.lines]:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -133,7 +153,7 @@ class ClockSampler:
                     reasons.add(name)
         sm.sort()
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "window": window}
 
 
 def _dist():
@@ -321,15 +341,18 @@ def run_ours(args, wl):
     l0 = eng.launches
     start = torch.cuda.Event(enable_timing=True)
     stop = torch.cuda.Event(enable_timing=True)
+    if sampler:
+        sampler.mark(True)
     start.record(eng.stream)
     run(args.warmup, args.steps)
     stop.record(eng.stream)
     torch.cuda.synchronize()
+    if sampler:
+        sampler.mark(False)
     if sharded:
         dist.barrier()
     launches = eng.launches - l0
     ms = start.elapsed_time(stop)
-    clocks = sampler.stop() if sampler else None
     # ---- the iteration kernel's duration over the timed region: the streaming
     # kernels (k_chain, k_rows) time themselves on the device (first CTA start
     # to last CTA end, %globaltimer) and count improved rows, per iteration,
@@ -346,6 +369,7 @@ def run_ours(args, wl):
     kms, kn = ctypes.c_double(), ctypes.c_int64()
     _lib.check(L.psso_profile_read(eng.ctx, ctypes.byref(kms), ctypes.byref(kn)))
     L.psso_profile(eng.ctx, 0)
+    clocks = sampler.stop() if sampler else None
     eng.check()
     kname = L.psso_kernel_name(eng.ctx).decode()
     dev_timed = s_n.value == nstat and nstat > 0
