@@ -92,3 +92,26 @@ def test_oracle_is_not_imported_by_the_product():
         assert "from oracle" not in text and "import oracle" not in text, py
     for src in list(pkg.rglob("*.cu")) + list(pkg.rglob("*.cuh")):
         assert "oracle" not in src.read_text(), src
+
+
+def test_nccl_resolved_at_run_time_and_comm_arguments_checked():
+    """libpsso.so has no link-time NCCL dependency: the communicator entry points
+    dlopen the process's libnccl.so.2 (torch's).  No GPU needed for the unique id."""
+    import subprocess
+
+    pytest.importorskip("torch")  # loads the bundled libnccl.so.2 into the process
+    from paper_2110_01470_b200 import _lib
+
+    deps = subprocess.run(["ldd", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "libnccl" not in deps
+    L = _lib.load()
+    uid = (ctypes.c_ubyte * 128)()
+    assert L.psso_nccl_unique_id(uid) == _lib.PSSO_OK
+    assert any(bytes(uid))
+    comm = ctypes.c_void_p()
+    assert L.psso_comm_create(uid, 2, 2, ctypes.byref(comm)) == _lib.PSSO_E_INVALID  # rank >= nranks
+    assert L.psso_comm_create(None, 1, 0, ctypes.byref(comm)) == _lib.PSSO_E_INVALID
+    assert L.psso_attach_comm(None, None) == _lib.PSSO_E_INVALID
+    assert L.psso_run_sharded(None, 0, 1) == _lib.PSSO_E_INVALID
+    st = ctypes.c_int64()
+    assert L.psso_batch_failure(ctypes.byref(st), None, None, None) == _lib.PSSO_OK and st.value == -1
