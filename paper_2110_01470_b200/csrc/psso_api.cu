@@ -772,6 +772,10 @@ TileParams tile_params(psso_ctx* c, int mode, int64_t t, const int64_t* t_dev, b
   p.seed = c->cfg.seed;
   p.Kw = c->Kw; p.Kp = c->Kp; p.Kg = c->Kg;
   p.Kw32 = c->Kw32; p.Kp32 = c->Kp32; p.Kg32 = c->Kg32;
+  p.Kw32u = (uint32_t)std::min<uint64_t>(c->Kw32, 0xFFFFFFFFull);
+  p.Kp32u = (uint32_t)std::min<uint64_t>(c->Kp32, 0xFFFFFFFFull);
+  p.Kg32u = (uint32_t)std::min<uint64_t>(c->Kg32, 0xFFFFFFFFull);
+  p.K32on = (c->Kw32 >> 32 ? 0u : 1u) | (c->Kp32 >> 32 ? 0u : 2u) | (c->Kg32 >> 32 ? 0u : 4u);
   p.var_min = c->cfg.var_min;
   p.span = c->cfg.var_max - c->cfg.var_min;
   p.span53 = std::ldexp(p.span, -53);
