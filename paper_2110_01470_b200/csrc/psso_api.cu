@@ -401,12 +401,17 @@ __global__ void __launch_bounds__(GB_THREADS) k_apply(const __grid_constant__ Gb
 // virtual ranks on one GPU), then raises its flag in each buffer with a
 // system-scope release; k_apply_p2p waits for all R flags of its own buffer
 // (system-scope acquire) and applies the selection exactly like k_apply.
-__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// One rank (R == 1): the exchange buffer is touched by this GPU only, so the
+// flags need GPU scope; any peer (another GPU, or another process's context)
+// needs system scope.
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v, bool sys) {
+  if (sys) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  else asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p, bool sys) {
   unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  if (sys) asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  else asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 
@@ -432,7 +437,7 @@ __device__ __forceinline__ void publish_body(const unsigned char* cand, unsigned
     // barrier, and release is cumulative: no separate system-wide fence (which
     // measured ~5 us per exchange) is needed
     for (int q = 0; q < R; ++q)
-      st_release_sys_u64(reinterpret_cast<unsigned long long*>(bufs[q]) + slot, epoch);
+      st_release_u64(reinterpret_cast<unsigned long long*>(bufs[q]) + slot, epoch, R > 1);
   }
 }
 
@@ -471,7 +476,7 @@ __global__ void __launch_bounds__(GB_THREADS) k_apply_p2p(const __grid_constant_
   if (threadIdx.x == 0) {
     const unsigned long long* flags = reinterpret_cast<const unsigned long long*>(buf) + par * R;
     for (int q = 0; q < R; ++q)
-      while (ld_acquire_sys_u64(flags + q) < epoch) __nanosleep(32);
+      while (ld_acquire_u64(flags + q, R > 1) < epoch) __nanosleep(32);
     double bf = CUDART_INF;
     int64_t bi = INT64_MAX;
     int w = 0;
