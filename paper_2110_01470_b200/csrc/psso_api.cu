@@ -299,9 +299,12 @@ __global__ void __launch_bounds__(GB_THREADS) k_gbest(const __grid_constant__ Gb
   }
 }
 
-// Local stage 2 for sharded runs: this rank's (p_f, index, row) record.
+// Local stage 2 for sharded runs: this rank's (p_f, index, row) record,
+// written to `n` destinations (dst[q] + off): the local record, or straight
+// into every rank's exchange buffer slot (the P2P device loop).
 template <typename T>
-__device__ __forceinline__ void local_cand_body(const GbParams& g, unsigned char* rec) {
+__device__ __forceinline__ void local_cand_to(const GbParams& g, unsigned char* const* dst, int n,
+                                              int64_t off) {
   __shared__ double sf[GB_THREADS / 32];
   __shared__ int64_t si[GB_THREADS / 32];
   double bf;
@@ -309,12 +312,12 @@ __device__ __forceinline__ void local_cand_body(const GbParams& g, unsigned char
   block_argmin<T>(g.slot_f, g.slot_i, g.nslots, bf, bi, sf, si);
   if (bi != INT64_MAX) {
     const T* src = reinterpret_cast<const T*>(g.P) + (bi - g.row_lo) * (int64_t)g.D;
-    T* dst = reinterpret_cast<T*>(rec + REC_HDR);
-    for (int j = threadIdx.x; j < g.D; j += blockDim.x) dst[j] = src[j];
+    for (int j = threadIdx.x; j < g.D; j += blockDim.x) {
+      const T v = src[j];
+      for (int q = 0; q < n; ++q) reinterpret_cast<T*>(dst[q] + off + REC_HDR)[j] = v;
+    }
   }
   if (threadIdx.x == 0) {
-    *reinterpret_cast<double*>(rec) = bf;
-    *reinterpret_cast<int64_t*>(rec + 8) = bi;
     const unsigned long long key = g.bad ? *g.bad : ~0ull;
     double v = 0.0;
     if (key != ~0ull) {
@@ -322,9 +325,19 @@ __device__ __forceinline__ void local_cand_body(const GbParams& g, unsigned char
       if (g.sol_f && i >= g.row_lo && i < g.row_hi) v = g.sol_f[i - g.row_lo];  // the owner's
       else if (g.bad_val) v = *g.bad_val;                       // learnt from an exchange
     }
-    *reinterpret_cast<unsigned long long*>(rec + 16) = key;
-    *reinterpret_cast<double*>(rec + 24) = v;
+    for (int q = 0; q < n; ++q) {
+      unsigned char* rec = dst[q] + off;
+      *reinterpret_cast<double*>(rec) = bf;
+      *reinterpret_cast<int64_t*>(rec + 8) = bi;
+      *reinterpret_cast<unsigned long long*>(rec + 16) = key;
+      *reinterpret_cast<double*>(rec + 24) = v;
+    }
   }
+}
+
+template <typename T>
+__device__ __forceinline__ void local_cand_body(const GbParams& g, unsigned char* rec) {
+  local_cand_to<T>(g, &rec, 1, 0);
 }
 
 template <typename T>
@@ -456,9 +469,18 @@ __global__ void __launch_bounds__(GB_THREADS) k_local_cand_publish(const __grid_
                                                                    unsigned char* const* bufs, int R,
                                                                    int rank, int64_t rec_bytes,
                                                                    int64_t flag_bytes) {
-  local_cand_body<T>(g, rec);
-  __syncthreads();  // the record (global, written by this block) is complete
-  publish_body(rec, bufs, R, rank, p2p_epoch(0, g.t_dev), rec_bytes, flag_bytes);
+  (void)rec;
+  const unsigned long long epoch = p2p_epoch(0, g.t_dev);
+  const int slot = (int)(epoch & 1) * R + rank;  // records double-buffered by epoch parity
+  // the record straight into this rank's slot of every buffer (R <= 64 ranks)
+  __shared__ unsigned char* dst[64];
+  for (int q = threadIdx.x; q < R && q < 64; q += blockDim.x) dst[q] = bufs[q];
+  __syncthreads();
+  local_cand_to<T>(g, dst, R < 64 ? R : 64, flag_bytes + (int64_t)slot * rec_bytes);
+  __syncthreads();  // every store of the record precedes the releases (cumulativity)
+  if (threadIdx.x == 0)
+    for (int q = 0; q < R; ++q)
+      st_release_u64(reinterpret_cast<unsigned long long*>(bufs[q]) + slot, epoch, R > 1);
 }
 
 template <typename T>
@@ -1961,6 +1983,7 @@ int psso_run_p2p(psso_ctx* c, int64_t t0, int64_t niter, void* const* peer_bufs,
   if (int rc = need_bound(c)) return rc;
   if (!peer_bufs || !my_buf || nranks < 1 || rank < 0 || rank >= nranks || t0 < 0 || niter < 0)
     return fail(c, PSSO_E_INVALID, "bad p2p loop arguments");
+  if (nranks > 64) return fail(c, PSSO_E_UNSUPPORTED, "the P2P device loop takes up to 64 ranks");
   if (!c->cand) CK(c, cudaMalloc(&c->cand, (size_t)psso_candidate_bytes(&c->cfg)));
   if (c->pgraph && (c->pg_peers != peer_bufs || c->pg_buf != my_buf || c->pg_R != nranks || c->pg_rank != rank)) {
     cudaGraphExecDestroy(c->pgraph);
