@@ -277,6 +277,8 @@ template <typename T>
 __global__ void __launch_bounds__(GB_THREADS) k_gbest(const __grid_constant__ GbParams g) {
   __shared__ double sf[GB_THREADS / 32];
   __shared__ int64_t si[GB_THREADS / 32];
+  pdl_trigger();
+  pdl_wait();
   double bf;
   int64_t bi;
   block_argmin<T>(g.slot_f, g.slot_i, g.nslots, bf, bi, sf, si);
@@ -827,10 +829,30 @@ TileParams tile_params(psso_ctx* c, int mode, int64_t t, const int64_t* t_dev, b
   return p;
 }
 
+// A launch that may overlap its predecessor's drain (PSSO_PDL); only kernels
+// that read predecessor output behind griddepcontrol.wait are launched so.
+cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t s) {
+  cudaLaunchConfig_t lc = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.gridDim = grid;
+  lc.blockDim = block;
+  lc.dynamicSmemBytes = smem;
+  lc.stream = s;
+  lc.attrs = at;
+  lc.numAttrs = PSSO_PDL ? 1 : 0;
+  return cudaLaunchKernelExC(&lc, fn, args);
+}
+
 int launch_tile(psso_ctx* c, const TileParams& p, bool fused = false) {
   void* args[] = {(void*)&p};
-  CK(c, cudaLaunchKernel(fused ? c->fused_fn : c->tile_fn, dim3(fused ? c->fused_grid : c->grid),
-                         dim3(NT), args, fused ? c->LF.smem : c->L.smem, c->stream));
+  if (fused && (c->chain || c->rows_w)) {  // k_chain / k_rows wait on their predecessor
+    CK(c, launch_pdl(c->fused_fn, dim3(c->fused_grid), dim3(NT), args, c->LF.smem, c->stream));
+  } else {
+    CK(c, cudaLaunchKernel(fused ? c->fused_fn : c->tile_fn, dim3(fused ? c->fused_grid : c->grid),
+                           dim3(NT), args, fused ? c->LF.smem : c->L.smem, c->stream));
+  }
   c->launches++;
   return PSSO_OK;
 }
@@ -862,7 +884,7 @@ GbParams gb_params(psso_ctx* c, int64_t t, int64_t* t_dev, int is_init, int nslo
 int launch_gbest(psso_ctx* c, const GbParams& g) {
   void* args[] = {(void*)&g};
   const void* fn = c->cfg.dtype == PSSO_F64 ? (const void*)k_gbest<double> : (const void*)k_gbest<float>;
-  CK(c, cudaLaunchKernel(fn, dim3(1), dim3(GB_THREADS), args, 0, c->stream));
+  CK(c, launch_pdl(fn, dim3(1), dim3(GB_THREADS), args, 0, c->stream));
   c->launches++;
   return PSSO_OK;
 }

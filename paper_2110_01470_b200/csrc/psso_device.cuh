@@ -123,6 +123,23 @@ struct TileParams {
 // reset by the gBest kernel of iteration t-1.  Recorded inside graph replays
 // too, where per-launch CUDA events cannot be.
 constexpr int STATS_CAP = 1024;
+
+// Programmatic dependent launch (PSSO_PDL): the iteration kernels and k_gbest
+// are launched so that each may be scheduled while its predecessor drains;
+// every read of a predecessor's output sits behind griddepcontrol.wait.
+#ifndef PSSO_PDL
+#define PSSO_PDL 0
+#endif
+__device__ __forceinline__ void pdl_wait() {
+#if PSSO_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_trigger() {
+#if PSSO_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -1410,6 +1427,8 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, sizeof(T) == 4 ? PSSO_CHAIN_MIN
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = lane & 7;
   T* scr = reinterpret_cast<T*>(smem + p.off_scr) + warp * 4 * (8 * M);
+  pdl_trigger();
+  pdl_wait();
   const unsigned long long t_start = gtimer();
   if (!INIT && p.bad && *(volatile unsigned long long*)p.bad != ~0ull) return;
 
@@ -1584,6 +1603,8 @@ __global__ void __launch_bounds__(256, PSSO_ROWS_JIT ? 3 : 2) k_rows(const __gri
   const int k = lane & 7, s = lane >> 3;
   const int slot = warp / W, sw = warp % W;
   const int mode = M_SEARCH | M_EVAL | M_PBEST | M_CAND | (p.mode & M_SOLF);
+  pdl_trigger();
+  pdl_wait();
   const unsigned long long t_start = gtimer();
   if (p.bad && *(volatile unsigned long long*)p.bad != ~0ull) return;
   const int64_t t = p.t_dev ? *p.t_dev : p.t_arg;
