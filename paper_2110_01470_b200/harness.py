@@ -38,6 +38,8 @@ __all__ = [
     "SweepReport",
     "parameter_sweep",
     "write_trajectories",
+    "write_trajectory_rows",
+    "read_trajectory_rows",
     "ExperimentConfig",
     "ExperimentReport",
     "SpeedupReport",
@@ -346,13 +348,31 @@ def compute_speedup(times_a, times_b, power_a: float, power_b: float,
 
 def write_trajectories(records: Sequence[RunRecord], path) -> None:
     """Sidecar with the per-iteration gBest curve of each run (reference harness.py:321-336)."""
+    write_trajectory_rows(((rec.run_id, str(rec.schedule), rec.function, t, float(value))
+                           for rec in records if rec.trajectory is not None
+                           for t, value in enumerate(rec.trajectory)), path)
+
+
+def write_trajectory_rows(rows, path) -> None:
+    """(run_id, schedule, function, t, value) rows in the sidecar format (reference harness.py:332-336)."""
     with open(path, "w", encoding="utf-8") as fh:
         fh.write(TRAJECTORY_HEADER + "\n")
-        for rec in records:
-            if rec.trajectory is None:
-                continue
-            for t, value in enumerate(rec.trajectory):
-                fh.write(f"{rec.run_id} {rec.schedule} {rec.function} {t} {float(value)!r}\n")
+        for run_id, schedule, function, t, value in rows:
+            fh.write(f"{run_id} {schedule} {function} {t} {float(value)!r}\n")
+
+
+def read_trajectory_rows(path) -> list:
+    """The sidecar's rows back as (run_id, schedule, function, t, value) (reference harness.py:339-351)."""
+    rows = []
+    with open(path, encoding="utf-8") as fh:
+        for line in fh:
+            line = line.strip()
+            if line and not line.startswith("#"):
+                rid, sched, fn, t, value = line.split()
+                rows.append((int(rid), sched, fn, int(t), float(value)))
+    if not rows:
+        raise ValueError(f"no trajectory rows in {path}")
+    return rows
 
 
 @dataclass

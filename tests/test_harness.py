@@ -169,3 +169,25 @@ def test_per_run_timing_protocol():
     assert [r.best_fitness for r in rep.records] == [r.best_fitness for r in batched.records]
     assert rep.metadata["wall_time_s"].startswith("per run")
     assert all(r.wall_time_s > 0 for r in rep.records)  # each run timed on its own
+
+
+def test_trajectory_sidecar_round_trip_matches_reference_format(tmp_path):
+    """write_trajectories / read_trajectory_rows: the reference sidecar format (harness.py:318-351)."""
+    import numpy as np
+
+    from paper_2110_01470_b200.records import RunRecord
+
+    recs = [RunRecord(run_id=k, schedule=ScheduleKind.PARALLEL, function="f5", nsol=4, nvar=3,
+                      niter=3, cw=0.3, cp=0.6, cg=0.8, seed=k, best_fitness=1.0 / (k + 1),
+                      wall_time_s=0.1, best_position=np.zeros(3),
+                      trajectory=np.array([3.0, 2.5, 1.0 / (k + 3)])) for k in range(2)]
+    p = tmp_path / "t.txt"
+    H.write_trajectories(recs, p)
+    text = p.read_text().splitlines()
+    assert text[0] == "# columns: run_id schedule function iteration gbest_fitness"
+    assert text[1] == "0 parallel f5 0 3.0"
+    rows = H.read_trajectory_rows(p)
+    assert len(rows) == 6 and rows[-1] == (1, "parallel", "f5", 2, 0.25)
+    with pytest.raises(ValueError):
+        (tmp_path / "e.txt").write_text("# columns\n")
+        H.read_trajectory_rows(tmp_path / "e.txt")
