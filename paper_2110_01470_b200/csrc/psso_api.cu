@@ -247,6 +247,28 @@ __device__ __forceinline__ void reset_stats(unsigned long long* stats, int64_t t
 // (core.py:190-193 over the whole swarm, not per shard).
 constexpr int64_t REC_HDR = 32;  // f64 p_f | i64 index | u64 non-finite key | f64 its value | row
 
+// Row copy by one CTA with the loads batched ahead of the stores: a plain
+// `dst[j] = src[j]` loop issues one load, waits for it, stores, and repeats --
+// for C5's 4096-element rows that was 16 dependent HBM round trips per
+// thread (k_gbest took ~10 us per iteration).  `fn(j, v)` receives each element.
+template <typename T, typename F>
+__device__ __forceinline__ void copy_row(const T* __restrict__ src, int D, F&& fn) {
+  constexpr int U = 16;
+  for (int base = 0; base < D; base += U * (int)blockDim.x) {
+    T v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = base + u * (int)blockDim.x + (int)threadIdx.x;
+      if (j < D) v[u] = __ldcg(src + j);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = base + u * (int)blockDim.x + (int)threadIdx.x;
+      if (j < D) fn(j, v[u]);
+    }
+  }
+}
+
 template <typename T>
 __device__ void block_argmin(const double* f, const int64_t* idx, int n, double& bf, int64_t& bi,
                              double* sf, int64_t* si) {
@@ -287,7 +309,7 @@ __global__ void __launch_bounds__(GB_THREADS) k_gbest(const __grid_constant__ Gb
   if (take) {
     const T* src = reinterpret_cast<const T*>(g.P) + (bi - g.row_lo) * (int64_t)g.D;
     T* dst = reinterpret_cast<T*>(g.gbest);
-    for (int j = threadIdx.x; j < g.D; j += blockDim.x) dst[j] = src[j];
+    copy_row<T>(src, g.D, [&](int j, T v) { dst[j] = v; });
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -314,10 +336,9 @@ __device__ __forceinline__ void local_cand_to(const GbParams& g, unsigned char* 
   block_argmin<T>(g.slot_f, g.slot_i, g.nslots, bf, bi, sf, si);
   if (bi != INT64_MAX) {
     const T* src = reinterpret_cast<const T*>(g.P) + (bi - g.row_lo) * (int64_t)g.D;
-    for (int j = threadIdx.x; j < g.D; j += blockDim.x) {
-      const T v = src[j];
+    copy_row<T>(src, g.D, [&](int j, T v) {
       for (int q = 0; q < n; ++q) reinterpret_cast<T*>(dst[q] + off + REC_HDR)[j] = v;
-    }
+    });
   }
   if (threadIdx.x == 0) {
     const unsigned long long key = g.bad ? *g.bad : ~0ull;
@@ -403,7 +424,7 @@ __global__ void __launch_bounds__(GB_THREADS) k_apply(const __grid_constant__ Gb
   if (take_s) {
     const T* src = reinterpret_cast<const T*>(recs + winner * rec_bytes + REC_HDR);
     T* dst = reinterpret_cast<T*>(g.gbest);
-    for (int j = threadIdx.x; j < g.D; j += blockDim.x) dst[j] = src[j];
+    copy_row<T>(src, g.D, [&](int j, T v) { dst[j] = v; });
   }
 }
 
@@ -527,7 +548,7 @@ __global__ void __launch_bounds__(GB_THREADS) k_apply_p2p(const __grid_constant_
   if (take_s) {
     const T* src = reinterpret_cast<const T*>(recs + winner * rec_bytes + REC_HDR);
     T* dst = reinterpret_cast<T*>(g.gbest);
-    for (int j = threadIdx.x; j < g.D; j += blockDim.x) dst[j] = __ldcg(src + j);
+    copy_row<T>(src, g.D, [&](int j, T v) { dst[j] = v; });
   }
 }
 
@@ -620,11 +641,10 @@ __global__ void k_seq_commit(T* X, T* P, const T* Xn, const double* fn, double* 
     const double f = fn[r];
     const bool imp = isfinite(f) && f <= p_f[r];
     const T* src = Xn + r * (int64_t)D;
-    for (int j = threadIdx.x; j < D; j += blockDim.x) {
-      const T v = src[j];
+    copy_row<T>(src, D, [&](int j, T v) {
       X[r * (int64_t)D + j] = v;
       if (imp) P[r * (int64_t)D + j] = v;
-    }
+    });
     __syncthreads();  // every thread read p_f[r] before it moves
     if (threadIdx.x == 0) {
       if (sol_f) sol_f[r] = f;
@@ -644,7 +664,7 @@ __global__ void k_seq_move(T* gbest, const T* Xn, const double* fn, double* g_f,
   if (threadIdx.x == 0) stop = ev < N && !isfinite(fn[ev]);
   __syncthreads();
   if (ev < N && !stop)
-    for (int j = threadIdx.x; j < D; j += blockDim.x) gbest[j] = Xn[ev * (int64_t)D + j];
+    copy_row<T>(Xn + ev * (int64_t)D, D, [&](int j, T v) { gbest[j] = v; });
   if (threadIdx.x == 0) {
     if (passes) *passes += 1;
     if (stop) {
