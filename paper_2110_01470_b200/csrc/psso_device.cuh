@@ -1618,7 +1618,15 @@ __global__ void __launch_bounds__(256, PSSO_ROWS_JIT ? 3 : 2) k_rows(const __gri
   }
   if constexpr (!PSSO_ROWS_JIT) {  // gbest padded by 8 elements per leaf: the segments' reads hit disjoint banks
     const T* g = reinterpret_cast<const T*>(p.gbest);
-    for (int j = tid; j < D; j += 256) gb[j + ((j >> 7) << 3)] = g[j];
+    constexpr int U = D / 256;  // loads batched ahead of the stores (not one round trip each)
+    T v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = g[tid + 256 * u];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = tid + 256 * u;
+      gb[j + ((j >> 7) << 3)] = v[u];
+    }
   }
   const int jb = 512 * sw + 128 * s + k;  // this lane's first element; j = jb + 8m
   const T* gbl = PSSO_ROWS_JIT ? reinterpret_cast<const T*>(p.gbest)  // gbest of this lane's leaf: gbl[j]
