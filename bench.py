@@ -310,8 +310,16 @@ def run_ours(args, wl):
     es = 8 if dtype == "float64" else 4
     drv = ex = None
     if sharded:
-        ex = (P2PExchange([eng], distributed=True) if args.exchange == "p2p"
-              else NcclExchange(eng) if args.exchange == "nccl" else ProcessGroupExchange())
+        if args.exchange == "nccl":
+            try:
+                ex = NcclExchange(eng)
+            except Exception as e:  # e.g. no loadable libnccl: every rank falls back alike
+                print(f"bench: library NCCL communicator unavailable ({e}); using the "
+                      "torch.distributed all-gather", file=sys.stderr, flush=True)
+                args.exchange = "collective"
+        if ex is None:
+            ex = (P2PExchange([eng], distributed=True) if args.exchange == "p2p"
+                  else ProcessGroupExchange())
         drv = ShardedDriver([eng], ex, ws)
 
     def run(t0, n):
