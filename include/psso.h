@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define PSSO_ABI_VERSION 1
+#define PSSO_ABI_VERSION 2  /* 2: 32-byte candidate header, gBest index, communicators, statistics */
 
 /* status codes */
 #define PSSO_OK 0

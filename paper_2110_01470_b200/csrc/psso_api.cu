@@ -1118,7 +1118,7 @@ cudaError_t pool_alloc(void** p, size_t bytes, cudaStream_t s) {
 
 extern "C" {
 
-const char* psso_version(void) { return "psso-b200 1 (sm_100a)"; }
+const char* psso_version(void) { return "psso-b200 2 (sm_100a)"; }
 
 const char* psso_kernel_name(const psso_ctx* ctx) { return ctx ? ctx->kname.c_str() : ""; }
 
