@@ -1157,11 +1157,14 @@ __device__ __forceinline__ const double* stage_aux(const double* aux, int D) {
 // x holds the loaded positions, pv the pbests unless INIT).  Positions, X
 // store, fitness in numpy order, pbest/p_f/sol_f bookkeeping and the
 // lexicographic candidate.  The whole warp must call it (shuffles).
-template <typename T, int FN, int RNG, int M, bool INIT, bool FULL, bool RES = false>
+// PVJIT: the pbests are read at their use from `pjit` (a shared-memory row,
+// k_swarm's resident swarm) instead of from the pv registers.
+template <typename T, int FN, int RNG, int M, bool INIT, bool FULL, bool RES = false, bool PVJIT = false>
 __device__ __forceinline__ bool chain_step(const TileParams& p, const ChainEnv& ev, const T* gb,
                                            const uint64_t* xg, T* scr, int64_t r, bool rv,
                                            T (&x)[M], const T (&pv)[M], double pf_row,
-                                           double& best_f, int64_t& best_i, int& best_new) {
+                                           double& best_f, int64_t& best_i, int& best_new,
+                                           const T* pjit = nullptr) {
   using N = Num<T>;
   const int lane = threadIdx.x & 31, k = lane & 7, seg = lane & ~7;
   const int D = ev.D;
@@ -1246,11 +1249,11 @@ __device__ __forceinline__ bool chain_step(const TileParams& p, const ChainEnv& 
         const uint64_t kb = mix64_tail<(M <= 8 || sizeof(T) == 8)>(xb ^ gx) >> 11;
         const double fresh = __dadd_rn(p.var_min, fresh_offset<(M <= 8 || sizeof(T) == 8)>(xf ^ gx, p.span64));
         v = x[m];
-        v = kb >= p.Kw ? pv[m] : v;
+        v = kb >= p.Kw ? (PVJIT ? (j < D ? pjit[j] : (T)0) : pv[m]) : v;
         v = kb >= p.Kp ? gb[j] : v;
         v = kb >= p.Kg ? (T)fresh : v;
       } else {
-        v = philox_select<T>(p, w, m & 1, x[m], pv[m], gb[j]);
+        v = philox_select<T>(p, w, m & 1, x[m], PVJIT ? (j < D ? pjit[j] : (T)0) : pv[m], gb[j]);
       }
       x[m] = v;
       if (rv && (FULL || j < D)) st_row<T, RES>(xr + j, v);
@@ -1681,7 +1684,6 @@ __global__ void __launch_bounds__(256, PSSO_ROWS_JIT ? 3 : 2) k_rows(const __gri
       wphase ^= 1;
       const T* xs = reinterpret_cast<const T*>(wbuf + s * RS);
       const T* ps = reinterpret_cast<const T*>(wbuf + 4 * RS + s * RS);
-      auto pbest = [&](int m) -> T { return PSSO_ROWS_JIT ? ps[k + 8 * m] : pv[PSSO_ROWS_JIT ? 0 : m]; };
       if constexpr (!PSSO_ROWS_JIT) {
 #pragma unroll
         for (int m = 0; m < M; ++m) {
@@ -1695,6 +1697,7 @@ __global__ void __launch_bounds__(256, PSSO_ROWS_JIT ? 3 : 2) k_rows(const __gri
 #pragma unroll
         for (int m = 0; m < M; ++m) x[m] = xs[k + 8 * m];
       }
+      auto pbest = [&](int m) -> T { return PSSO_ROWS_JIT ? ps[k + 8 * m] : pv[PSSO_ROWS_JIT ? 0 : m]; };
 
       // ---- positions (core.py:138-173; see k_chain), each followed at once
       // by its objective terms and the in-order chain adds of leaf 4sw+s

@@ -32,6 +32,9 @@
 
 namespace psso {
 
+#ifndef PSSO_SWARM_PVJIT
+#define PSSO_SWARM_PVJIT 0  // resident swarms: pbests read from shared memory at their use
+#endif
 #ifndef PSSO_SWARM_NT
 #define PSSO_SWARM_NT 512  // 16 warps: four per scheduler to hide the chain latency
 #endif
@@ -369,18 +372,25 @@ __global__ void __launch_bounds__(PSSO_SWARM_NT, 1)
       const double pf_row = ev.p_f[rl];
       const T* xl = reinterpret_cast<const T*>(ev.X) + rl * (int64_t)D;
       const T* pl = Pb + rl * (int64_t)D;
-      T x[M], pv[M];
+      T x[M], pv[PSSO_SWARM_PVJIT && RES ? 1 : M];
 #pragma unroll
       for (int m = 0; m < M; ++m) {
         const int j = k + 8 * m;
         x[m] = j < D ? xl[j] : (T)0;
-        pv[m] = j < D ? pl[j] : (T)0;
+        if constexpr (!(PSSO_SWARM_PVJIT && RES)) pv[m] = j < D ? pl[j] : (T)0;
       }
       // a segment past the last row reads the (clamped) last row, which the
       // valid segment of the same warp rewrites below: loads before stores
+      // (PVJIT: its pbest reads precede the row's pBest write-back, which
+      // follows the warp-synchronous fitness shuffles)
       __syncwarp();
-      chain_step<T, FN, RNG, M, false, false, RES>(p, ev, gb, xg, scr, r - r0, rv, x, pv, pf_row,
-                                                   best_f, best_i, best_new);
+      if constexpr (PSSO_SWARM_PVJIT && RES)
+        chain_step<T, FN, RNG, M, false, false, RES, true>(p, ev, gb, xg, scr, r - r0, rv, x, x, pf_row,
+                                                           best_f, best_i, best_new, pl);
+      else
+        chain_step<T, FN, RNG, M, false, false, RES>(p, ev, gb, xg, scr, r - r0, rv, x,
+                                                     reinterpret_cast<const T(&)[M]>(pv), pf_row,
+                                                     best_f, best_i, best_new);
     }
     stop = exchange(best_f, best_i, best_new, false, t);
     PSSO_TRACE(it, 3);
