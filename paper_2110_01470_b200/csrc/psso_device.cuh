@@ -1090,6 +1090,11 @@ __device__ __forceinline__ T chain_term1(T x, T nb, int e) {
 #ifndef PSSO_CHAIN_MINB_F32
 #define PSSO_CHAIN_MINB_F32 PSSO_CHAIN_MINB  // resident CTAs per SM for the fp32 chain kernels
 #endif
+#ifndef PSSO_SWARM_PVJIT
+#define PSSO_SWARM_PVJIT 1  // k_swarm / k_seq with resident rows: pbests read from shared memory at
+                            // their use (C2 f4 7.5 -> 6.8 us, f6 7.5 -> 7.2, f7 10.5 -> 10.2, C1 3.1 -> 3.0
+                            // per iteration)
+#endif
 #ifndef PSSO_CHAIN_PF
 #define PSSO_CHAIN_PF 1  // FULL iteration kernel: TMA prefetch of the next group
 #endif

@@ -163,15 +163,20 @@ __global__ void __launch_bounds__(PSSO_SEQ_NT, 1)
         const double pf_row = pf[rl - base];
         const T* xl = X + (rl - base) * (int64_t)D;
         const T* pl = P + (rl - base) * (int64_t)D;
-        T x[M], pv[M];
+        T x[M], pv[PSSO_SWARM_PVJIT && RES ? 1 : M];
 #pragma unroll
         for (int m = 0; m < M; ++m) {
           const int j = k + 8 * m;
           x[m] = j < D ? xl[j] : (T)0;
-          pv[m] = j < D ? pl[j] : (T)0;
+          if constexpr (!(PSSO_SWARM_PVJIT && RES)) pv[m] = j < D ? pl[j] : (T)0;
         }
-        chain_step<T, FN, RNG, M, false, false, true>(p, ev, gb, xg, scr, r - base, rv, x, pv, pf_row,
-                                                      best_f, best_i, best_new);
+        if constexpr (PSSO_SWARM_PVJIT && RES)  // pbests from the resident rows at their use
+          chain_step<T, FN, RNG, M, false, false, true, true>(p, ev, gb, xg, scr, r - base, rv, x, x,
+                                                              pf_row, best_f, best_i, best_new, pl);
+        else
+          chain_step<T, FN, RNG, M, false, false, true>(p, ev, gb, xg, scr, r - base, rv, x,
+                                                        reinterpret_cast<const T(&)[M]>(pv), pf_row,
+                                                        best_f, best_i, best_new);
       }
       __syncthreads();  // Xn / fn of the pass visible to the CTA
       // ---- this CTA's first event: non-finite (core.py:233) or a gbest move (core.py:236-241)

@@ -32,9 +32,6 @@
 
 namespace psso {
 
-#ifndef PSSO_SWARM_PVJIT
-#define PSSO_SWARM_PVJIT 0  // resident swarms: pbests read from shared memory at their use
-#endif
 #ifndef PSSO_SWARM_NT
 #define PSSO_SWARM_NT 512  // 16 warps: four per scheduler to hide the chain latency
 #endif
