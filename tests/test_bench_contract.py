@@ -111,3 +111,28 @@ def test_bench_sharded_nccl_graph_path_world_size_1():
     assert d["config"]["nsol"] == 1 << 24 and "NCCL" in d["config"]["parallelism"]
     assert d["roofline"]["kernel"].startswith("k_chain") and d["roofline"]["frac"] > 0.5
     assert d["e2e"]["value"] > 0
+
+
+@pytest.mark.gpu
+def test_bench_gpus_2_self_spawns_and_bootstraps_the_nccl_communicator():
+    """bench.py --gpus 2 without torchrun (self-spawn) on the one GPU of the box, gloo
+    process group: both ranks run the library's communicator bootstrap (rank 0's
+    ncclUniqueId over the process group, collective ncclCommInitRank), which NCCL
+    refuses for two ranks on one device -- every rank then falls back to the
+    torch.distributed all-gather alike and the run completes with n_gpus 2."""
+    import os
+
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    env = dict(os.environ, PSSO_BENCH_BACKEND="gloo")
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--steps", "6",
+                          "--warmup", "3", "--workload", "c3sphere", "--no-cpu"],
+                         cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [json.loads(ln) for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
+    assert out.stderr.count("library NCCL communicator unavailable") == 2  # both ranks, alike
+    assert "torch.distributed all-gather" in d["config"]["parallelism"]
