@@ -1207,7 +1207,7 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
       c->LF.off_red = PSSO_ROWS_JIT ? 0 : (int)align16((size_t)(D + D / 16) * es);  // gbest padded per leaf
       c->LF.off_leaf = c->LF.off_red + 128;  // leaf values [2][8/W][2*4W + 1] doubles
       c->LF.off_flag = c->LF.off_leaf + (int)align16(2 * (size_t)(8 / W) * (8 * W + 1) * 8);
-      c->LF.off_bar = (int)align16((size_t)c->LF.off_flag + 32);
+      c->LF.off_bar = (int)align16((size_t)c->LF.off_flag + 64);  // flags [2][8/W] ints
       c->LF.off_xs = (int)((c->LF.off_bar + 64 + 127) & ~127);
       c->LF.smem = (size_t)c->LF.off_xs + 8 * 8 * host_row_stride(es, 16);
     }

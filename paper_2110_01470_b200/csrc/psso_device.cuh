@@ -1596,6 +1596,11 @@ __host__ __device__ constexpr bool rows_fn() {
 #ifndef PSSO_ROWS_JIT
 #define PSSO_ROWS_JIT 0
 #endif
+// PSSO_ROWS_ONEFINISH: only the row's first warp combines the leaves and
+// evaluates the objective; the others take its decision after a second barrier.
+#ifndef PSSO_ROWS_ONEFINISH
+#define PSSO_ROWS_ONEFINISH 0
+#endif
 template <typename T, int FN, int RNG, int W>
 __global__ void __launch_bounds__(256, PSSO_ROWS_JIT ? 3 : 2) k_rows(const __grid_constant__ TileParams p) {
   using N = Num<T>;
@@ -1606,6 +1611,7 @@ __global__ void __launch_bounds__(256, PSSO_ROWS_JIT ? 3 : 2) k_rows(const __gri
   double* red_f = reinterpret_cast<double*>(smem + p.off_red);
   int64_t* red_i = reinterpret_cast<int64_t*>(smem + p.off_red + 8 * NW);
   double* leafv = reinterpret_cast<double*>(smem + p.off_leaf);  // [2][RPC][2 NL + 1]
+  int* rflag = reinterpret_cast<int*>(smem + p.off_flag);          // [2][RPC] (PSSO_ROWS_ONEFINISH)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = lane & 7, s = lane >> 3;
@@ -1769,7 +1775,8 @@ __global__ void __launch_bounds__(256, PSSO_ROWS_JIT ? 3 : 2) k_rows(const __gri
     // a row combines the leaves itself, so nobody waits for a decision.
     __syncthreads();
 
-    if (rv) {  // every warp of the row: balanced tree over the 4W leaves (redundant, no 2nd barrier)
+    bool imp = false;
+    if (rv && (!PSSO_ROWS_ONEFINISH || sw == 0)) {  // balanced tree over the 4W leaves
       const T x0 = (T)lv[2 * NL];
       T s1 = (T)0, s2 = (T)0;
       if (lane < NL) {
@@ -1783,7 +1790,8 @@ __global__ void __launch_bounds__(256, PSSO_ROWS_JIT ? 3 : 2) k_rows(const __gri
       }
       // lanes < 4W hold the row sums after the butterfly; lane 0 decides for all
       const double f = finish<T, FN>(s1, s2, (T)1, D, &x0, p.probe_level);
-      const bool imp = __shfl_sync(0xffffffffu, (int)(f <= pf_row), 0) != 0;  // parallel.py:109
+      imp = __shfl_sync(0xffffffffu, (int)(f <= pf_row), 0) != 0;  // parallel.py:109
+      if (PSSO_ROWS_ONEFINISH && lane == 0) rflag[par * RPC + slot] = imp;
       if (sw == 0 && lane == 0) {
         if (!isfinite(f) && p.bad)
           atomicMin(p.bad, ((unsigned long long)(t + 1) << 40) | (unsigned long long)gi);
@@ -1793,11 +1801,15 @@ __global__ void __launch_bounds__(256, PSSO_ROWS_JIT ? 3 : 2) k_rows(const __gri
         nimp += imp ? 1 : 0;
         if (lex_less(pf, gi, best_f, best_i)) { best_f = pf; best_i = gi; }
       }
-      if (imp) {  // this warp's slice of pbests[i] = sol[i], from registers
-        T* pr = P + r * (int64_t)D;
+    }
+    if constexpr (PSSO_ROWS_ONEFINISH) {  // (B) the row's decision, from its first warp
+      __syncthreads();
+      imp = rv && rflag[par * RPC + slot];
+    }
+    if (imp) {  // this warp's slice of pbests[i] = sol[i], from registers
+      T* pr = P + r * (int64_t)D;
 #pragma unroll
-        for (int m = 0; m < M; ++m) stg_stream<T, 1>(pr + jb + 8 * m, VecT<T, 1>{{x[m]}});
-      }
+      for (int m = 0; m < M; ++m) stg_stream<T, 1>(pr + jb + 8 * m, VecT<T, 1>{{x[m]}});
     }
   }
 
