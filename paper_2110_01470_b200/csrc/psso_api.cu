@@ -486,24 +486,34 @@ __global__ void __launch_bounds__(GB_THREADS) k_publish(const unsigned char* can
 
 // the device loop's record + publish in one kernel: this rank's record (as
 // k_local_cand), then stored into every rank's buffer with the epoch flags
+// Up to 8 peers (a node's GPUs) travel by value in the launch parameters, so
+// the kernel starts without a dependent load of the peer table.
+struct PeerPtrs {
+  unsigned char* p[8];
+  int32_t n;  // 0: read the device table instead
+};
+
 template <typename T>
 __global__ void __launch_bounds__(GB_THREADS) k_local_cand_publish(const __grid_constant__ GbParams g,
-                                                                   unsigned char* rec,
-                                                                   unsigned char* const* bufs, int R,
-                                                                   int rank, int64_t rec_bytes,
+                                                                   unsigned char* const* bufs,
+                                                                   const __grid_constant__ PeerPtrs pp,
+                                                                   int R, int rank, int64_t rec_bytes,
                                                                    int64_t flag_bytes) {
-  (void)rec;
   const unsigned long long epoch = p2p_epoch(0, g.t_dev);
   const int slot = (int)(epoch & 1) * R + rank;  // records double-buffered by epoch parity
   // the record straight into this rank's slot of every buffer (R <= 64 ranks)
-  __shared__ unsigned char* dst[64];
-  for (int q = threadIdx.x; q < R && q < 64; q += blockDim.x) dst[q] = bufs[q];
-  __syncthreads();
+  __shared__ unsigned char* dst_s[64];
+  unsigned char* const* dst = pp.p;
+  if (pp.n == 0) {
+    for (int q = threadIdx.x; q < R && q < 64; q += blockDim.x) dst_s[q] = bufs[q];
+    __syncthreads();
+    dst = dst_s;
+  }
   local_cand_to<T>(g, dst, R < 64 ? R : 64, flag_bytes + (int64_t)slot * rec_bytes);
   __syncthreads();  // every store of the record precedes the releases (cumulativity)
   if (threadIdx.x == 0)
     for (int q = 0; q < R; ++q)
-      st_release_u64(reinterpret_cast<unsigned long long*>(bufs[q]) + slot, epoch, R > 1);
+      st_release_u64(reinterpret_cast<unsigned long long*>(dst[q]) + slot, epoch, R > 1);
 }
 
 template <typename T>
@@ -754,6 +764,9 @@ struct psso_ctx {
   const void* pg_peers;     // the arguments pgraph was captured with
   const void* pg_buf;
   int32_t pg_R, pg_rank;
+  PeerPtrs pp;              // psso_run_p2p's peer table by value (<= 8 ranks) ...
+  const void* pp_src;       // ... read from this device table
+  int32_t pp_R;
   std::string kname;     // the iteration kernel psso_run launches (psso_kernel_name)
   std::string err;
 };
@@ -2016,16 +2029,16 @@ int psso_apply_p2p(psso_ctx* c, int64_t t, const void* my_buf, int32_t nranks, u
 }
 
 // one P2P exchange step with t (and the epoch) from the device counter
-static int p2p_step_dev(psso_ctx* c, const void* peer_bufs, const void* my_buf, int32_t nranks,
-                        int32_t rank) {
+static int p2p_step_dev(psso_ctx* c, const void* peer_bufs, const PeerPtrs& pp, const void* my_buf,
+                        int32_t nranks, int32_t rank) {
   if (int rc = launch_fused(c, 0, c->t_dev)) return rc;
   const int64_t rb = psso_candidate_bytes(&c->cfg), fb = (int64_t)align16((size_t)nranks * 16);
   GbParams gl = gb_params(c, 0, c->t_dev, 0, c->fused_grid);
   if (c->cfg.dtype == PSSO_F64)
-    k_local_cand_publish<double><<<1, GB_THREADS, 0, c->stream>>>(gl, c->cand, (unsigned char* const*)peer_bufs,
+    k_local_cand_publish<double><<<1, GB_THREADS, 0, c->stream>>>(gl, (unsigned char* const*)peer_bufs, pp,
                                                                   nranks, rank, rb, fb);
   else
-    k_local_cand_publish<float><<<1, GB_THREADS, 0, c->stream>>>(gl, c->cand, (unsigned char* const*)peer_bufs,
+    k_local_cand_publish<float><<<1, GB_THREADS, 0, c->stream>>>(gl, (unsigned char* const*)peer_bufs, pp,
                                                                  nranks, rank, rb, fb);
   GbParams g = gb_params(c, 0, c->t_dev, 0, 0);
   if (c->cfg.dtype == PSSO_F64)
@@ -2050,6 +2063,16 @@ int psso_run_p2p(psso_ctx* c, int64_t t0, int64_t niter, void* const* peer_bufs,
     c->pgraph = nullptr;
   }
   if (niter == 0) return PSSO_OK;
+  if (c->pp_src != peer_bufs || c->pp_R != nranks) {  // the peer table by value for up to 8 ranks,
+    std::memset(&c->pp, 0, sizeof c->pp);               // read once per table (never during capture)
+    if (nranks <= 8) {
+      CK(c, cudaMemcpy(c->pp.p, peer_bufs, sizeof(void*) * (size_t)nranks, cudaMemcpyDeviceToHost));
+      c->pp.n = nranks;
+    }
+    c->pp_src = peer_bufs;
+    c->pp_R = nranks;
+  }
+  const PeerPtrs& pp = c->pp;
   k_set<<<1, 1, 0, c->stream>>>(c->t_dev, t0);
   c->launches++;
   int64_t done = 0;
@@ -2060,7 +2083,7 @@ int psso_run_p2p(psso_ctx* c, int64_t t0, int64_t niter, void* const* peer_bufs,
       CK(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
       const int64_t saved = c->launches;
       for (int k = 0; k < GRAPH_CHUNK; ++k) {
-        int rc = p2p_step_dev(c, peer_bufs, my_buf, nranks, rank);
+        int rc = p2p_step_dev(c, peer_bufs, pp, my_buf, nranks, rank);
         if (rc) { cudaStreamEndCapture(c->stream, &gr); return rc; }
       }
       c->launches = saved;
@@ -2079,7 +2102,7 @@ int psso_run_p2p(psso_ctx* c, int64_t t0, int64_t niter, void* const* peer_bufs,
     }
   }
   for (; done < niter; ++done)  // same kernels, launched directly
-    if (int rc = p2p_step_dev(c, peer_bufs, my_buf, nranks, rank)) return rc;
+    if (int rc = p2p_step_dev(c, peer_bufs, pp, my_buf, nranks, rank)) return rc;
   return PSSO_OK;
 }
 
