@@ -1259,7 +1259,10 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
       return e != cudaSuccess ? cuda_fail(nullptr, e, "occupancy") : fail(nullptr, PSSO_E_UNSUPPORTED, "chain kernel cannot be resident");
     }
     const int64_t nctas = (rows + 4 * (NT / 32) - 1) / (4 * (NT / 32));
-    c->fused_grid = (int)std::min<int64_t>(nctas, (int64_t)per_sm_fused * c->num_sms);
+    int sms = c->num_sms;  // PSSO_FUSED_SMS (diagnostic): persistent grid over fewer SMs
+    if (const char* f = std::getenv("PSSO_FUSED_SMS"))
+      if (*f) sms = std::max(1, std::min(c->num_sms, std::atoi(f)));
+    c->fused_grid = (int)std::min<int64_t>(nctas, (int64_t)per_sm_fused * sms);
     c->init_grid = (int)std::min<int64_t>(nctas, (int64_t)per_sm_init * c->num_sms);
   }
   if (c->rows_w) {  // 8 / W rows per CTA round
