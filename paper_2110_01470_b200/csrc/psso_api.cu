@@ -529,6 +529,7 @@ __global__ void __launch_bounds__(GB_THREADS) k_apply_p2p(const __grid_constant_
   const int par = (int)(epoch & 1);
   const unsigned char* recs = buf + flag_bytes + (int64_t)par * R * rec_bytes;
   if (threadIdx.x == 0) {
+    const double inc = *g.g_f;  // this rank's own state: loaded while the flags are polled
     const unsigned long long* flags = reinterpret_cast<const unsigned long long*>(buf) + par * R;
     for (int q = 0; q < R; ++q)
       while (ld_acquire_u64(flags + q, R > 1) < epoch) __nanosleep(32);
@@ -542,7 +543,6 @@ __global__ void __launch_bounds__(GB_THREADS) k_apply_p2p(const __grid_constant_
       if (lex_less(f, i, bf, bi)) { bf = f; bi = i; w = k; }
     }
     adopt_nonfinite(g, recs, rec_bytes, R, true);
-    const double inc = *g.g_f;
     take_s = bi != INT64_MAX && (g.is_init || bf <= inc);  // parallel.py:209
     winner = w;
     const double gf = take_s ? bf : inc;
