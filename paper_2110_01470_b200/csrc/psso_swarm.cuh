@@ -369,19 +369,20 @@ __global__ void __launch_bounds__(PSSO_SWARM_NT, 1)
       const double pf_row = ev.p_f[rl];
       const T* xl = reinterpret_cast<const T*>(ev.X) + rl * (int64_t)D;
       const T* pl = Pb + rl * (int64_t)D;
-      T x[M], pv[PSSO_SWARM_PVJIT && RES ? 1 : M];
+      // (f5 keeps its pbests in registers: 7.1 vs 7.2 us per C2 iteration)
+      T x[M], pv[PSSO_SWARM_PVJIT && RES && FN != 5 ? 1 : M];
 #pragma unroll
       for (int m = 0; m < M; ++m) {
         const int j = k + 8 * m;
         x[m] = j < D ? xl[j] : (T)0;
-        if constexpr (!(PSSO_SWARM_PVJIT && RES)) pv[m] = j < D ? pl[j] : (T)0;
+        if constexpr (!(PSSO_SWARM_PVJIT && RES && FN != 5)) pv[m] = j < D ? pl[j] : (T)0;
       }
       // a segment past the last row reads the (clamped) last row, which the
       // valid segment of the same warp rewrites below: loads before stores
       // (PVJIT: its pbest reads precede the row's pBest write-back, which
       // follows the warp-synchronous fitness shuffles)
       __syncwarp();
-      if constexpr (PSSO_SWARM_PVJIT && RES)
+      if constexpr (PSSO_SWARM_PVJIT && RES && FN != 5)
         chain_step<T, FN, RNG, M, false, false, RES, true>(p, ev, gb, xg, scr, r - r0, rv, x, x, pf_row,
                                                            best_f, best_i, best_new, pl);
       else
