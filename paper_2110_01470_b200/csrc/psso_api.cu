@@ -1195,9 +1195,11 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
         // gbest past D in the branch-free select)
         c->LF.off_red = (int)align16((size_t)8 * M * es);
         c->LF.off_bar = (int)align16((size_t)c->LF.off_red + 128 + 64 * M);
-        c->LF.off_xs = (int)((c->LF.off_bar + 8 * nw + 127) & ~127);
+        c->LF.off_xs = (int)((c->LF.off_bar + 16 * nw + 127) & ~127);  // two mbarriers per warp
+        const bool db = PSSO_CHAIN_DB && 8 * M * es <= 512;  // chain_db<T, M>()
         c->LF.off_scr = (int)align16((size_t)c->LF.off_xs +
-                                     (full && PSSO_CHAIN_PF ? (size_t)nw * 8 * host_row_stride(es, M) : 0));
+                                     (full && PSSO_CHAIN_PF ? (size_t)nw * (db ? 2 : 1) * 8 *
+                                      host_row_stride(es, M) : 0));
         c->LF.smem = (size_t)c->LF.off_scr + (smem_fn ? (size_t)nw * 4 * (8 * M) * es : 0);
         c->init_smem = c->LF.smem;
       }

@@ -1119,6 +1119,12 @@ template <typename T>
 __host__ __device__ constexpr int row_pad() { return PSSO_ROW_PAD ? (sizeof(T) == 8 ? 64 : 32) : 0; }
 template <typename T, int M>
 __host__ __device__ constexpr int chain_row_stride() { return 8 * M * (int)sizeof(T) + row_pad<T>(); }
+// PSSO_CHAIN_DB: double-buffered prefetch for rows of at most 512 B (see k_chain)
+#ifndef PSSO_CHAIN_DB
+#define PSSO_CHAIN_DB 0
+#endif
+template <typename T, int M>
+__host__ __device__ constexpr bool chain_db() { return PSSO_CHAIN_DB && 8 * M * (int)sizeof(T) <= 512; }
 
 // Row store of the chain step: streaming global store, or a plain store when
 // the swarm is resident in shared memory (RES, k_swarm).
@@ -1484,10 +1490,16 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, sizeof(T) == 4 ? PSSO_CHAIN_MIN
   // without costing registers.
   constexpr bool PF = FULL && !INIT && PSSO_CHAIN_PF;
   constexpr int RS = chain_row_stride<T, M>();
-  uint64_t* wbar = reinterpret_cast<uint64_t*>(smem + p.off_bar) + warp;
-  unsigned char* wbuf = smem + p.off_xs + (size_t)warp * (8 * RS);
+  // DB: two buffers per warp (rows of <= 512 B: C4's fp64 M = 8, fp32 M = 16),
+  // so the pbests are read from the buffer at their use instead of being held
+  // in M registers, and the next group still streams in behind the current one
+  constexpr bool DB = PF && chain_db<T, M>();
+  uint64_t* wbar0 = reinterpret_cast<uint64_t*>(smem + p.off_bar) + 2 * warp;
+  unsigned char* wbuf0 = smem + p.off_xs + (size_t)warp * (DB ? 2 : 1) * (8 * RS);
+  uint64_t* wbar = wbar0;
+  unsigned char* wbuf = wbuf0;
   const int64_t gstride = (int64_t)gridDim.x * NW;
-  uint32_t wphase = 0;
+  uint32_t wphase = 0, wphase1 = 0;
   auto prefetch = [&](int64_t g) {  // whole warp calls; one lane issues both copies
     if (g >= ngroups) return;
     if (lane == 0) {
@@ -1509,14 +1521,16 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, sizeof(T) == 4 ? PSSO_CHAIN_MIN
   };
   if constexpr (PF) {
     if (lane == 0) {
-      mbar_init(wbar, 1);
+      mbar_init(wbar0, 1);
+      if constexpr (DB) mbar_init(wbar0 + 1, 1);
       mbar_fence_init();
     }
     __syncwarp();
     prefetch((int64_t)blockIdx.x * NW + warp);
   }
 
-  for (int64_t grp = (int64_t)blockIdx.x * NW + warp; grp < ngroups; grp += gstride) {
+  int it = 0;
+  for (int64_t grp = (int64_t)blockIdx.x * NW + warp; grp < ngroups; grp += gstride, ++it) {
     const int64_t r = 4 * grp + (lane >> 3);
     const bool rv = r < rows;
     // rows past the end (last group only) compute on a clamped row and store nothing
@@ -1525,8 +1539,25 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, sizeof(T) == 4 ? PSSO_CHAIN_MIN
     if (!INIT) pf_row = p.p_f[rl];
 
     T x[M];
-    T pv[M];
-    if constexpr (PF) {
+    T pv[DB ? 1 : M];
+    const T* ps_cur = nullptr;
+    if constexpr (DB) {
+      const int b = it & 1;  // this group's buffer; the other one takes the next group
+      uint32_t& ph = b ? wphase1 : wphase;
+      mbar_wait(wbar0 + b, ph);
+      ph ^= 1;
+      __syncwarp();  // the other buffer's reads (previous group) are done ...
+      fence_proxy_async();
+      wbar = wbar0 + (b ^ 1);
+      wbuf = wbuf0 + (b ^ 1) * (8 * RS);
+      prefetch(grp + gstride);  // ... before TMA refills it
+      const int sr = (int)(rl - 4 * grp);
+      const unsigned char* cur = wbuf0 + b * (8 * RS);
+      const T* xs = reinterpret_cast<const T*>(cur + sr * RS);
+      ps_cur = reinterpret_cast<const T*>(cur + 4 * RS + sr * RS);
+#pragma unroll
+      for (int m = 0; m < M; ++m) x[m] = xs[k + 8 * m];
+    } else if constexpr (PF) {
       mbar_wait(wbar, wphase);
       wphase ^= 1;
       const int sr = (int)(rl - 4 * grp);  // clamped row within the group
@@ -1535,7 +1566,7 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, sizeof(T) == 4 ? PSSO_CHAIN_MIN
 #pragma unroll
       for (int m = 0; m < M; ++m) {
         x[m] = xs[k + 8 * m];
-        pv[m] = ps[k + 8 * m];
+        pv[DB ? 0 : m] = ps[k + 8 * m];
       }
       __syncwarp();  // the whole buffer is in registers before it is refilled
       fence_proxy_async();
@@ -1548,20 +1579,26 @@ __global__ void __launch_bounds__(PSSO_CHAIN_NT, sizeof(T) == 4 ? PSSO_CHAIN_MIN
         const int j = k + 8 * m;
         if (FULL || j < ev.D) {
           x[m] = ldg_stream<T, 1>(xl + j).v[0];
-          pv[m] = ldg_stream<T, 1>(pl + j).v[0];
+          pv[DB ? 0 : m] = ldg_stream<T, 1>(pl + j).v[0];
         } else {
           x[m] = (T)0;
-          pv[m] = (T)0;
+          pv[DB ? 0 : m] = (T)0;
         }
       }
       __syncwarp();  // clamped last-row loads precede the valid segment's stores
     } else {
 #pragma unroll
-      for (int m = 0; m < M; ++m) pv[m] = (T)0;
+      for (int m = 0; m < M; ++m) pv[DB ? 0 : m] = (T)0;
     }
     int best_new = 0;
-    const bool imp = chain_step<T, FN, RNG, M, INIT, FULL>(p, ev, gb, xg, scr, r, rv, x, pv, pf_row,
-                                                           best_f, best_i, best_new);
+    bool imp;
+    if constexpr (DB)
+      imp = chain_step<T, FN, RNG, M, INIT, FULL, false, true>(p, ev, gb, xg, scr, r, rv, x, x, pf_row,
+                                                               best_f, best_i, best_new, ps_cur);
+    else
+      imp = chain_step<T, FN, RNG, M, INIT, FULL>(p, ev, gb, xg, scr, r, rv, x,
+                                                  reinterpret_cast<const T(&)[M]>(pv), pf_row,
+                                                  best_f, best_i, best_new);
     nimp += (imp && k == 0) ? 1 : 0;
   }
   cta_candidate<NW>(best_f, best_i, red_f, red_i, p.slot_f + blockIdx.x, p.slot_i + blockIdx.x);
