@@ -376,3 +376,18 @@ def test_sequential_resident_rows_equal_global_rows(fid, nsol, nvar, monkeypatch
     (a, ta), (b, tb) = outs
     assert np.array_equal(a.sol, b.sol) and np.array_equal(a.pbests, b.pbests)
     assert np.array_equal(a.p_f, b.p_f) and np.array_equal(ta, tb)
+
+
+@pytest.mark.parametrize("dtype,rng", [("float32", "reference"), ("float64", "philox"),
+                                       ("float32", "philox")])
+def test_sequential_long_rows_other_modes(dtype, rng):
+    """The device pass loop (nvar > 128) in fp32 and benchmark modes: a valid run --
+    monotone trajectory, positions in the box, gbest consistent with its fitness."""
+    fn = psso.make_function("f5", 300)
+    p = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=fn.var_min, var_max=fn.var_max, nsol=50,
+                       nvar=300, niter=20)
+    rec = psso.run_sequential(p, fn, seed=5, dtype=dtype, rng=rng)
+    assert np.all(np.diff(rec.trajectory) <= 0) and np.isfinite(rec.trajectory).all()
+    assert np.all(np.abs(rec.best_position) <= 5.12)
+    assert rec.best_fitness == pytest.approx(
+        fn(rec.best_position[None, :].astype(np.float64))[0], rel=1e-5 if dtype == "float32" else 1e-12)
