@@ -111,9 +111,10 @@ class ExperimentConfig:
     batched device job and gives every record the batch's loop time divided by
     the number of runs; True runs and times every replication on its own, the
     reference's protocol (harness.py:148-163), for speedup / RE comparisons
-    (harness.py:354-384).  ``workers``, ``layout``, ``block_size`` and
-    ``parallel_cells`` are accepted and have no effect on results, as in the
-    reference (cells are already batched on the device).
+    (harness.py:354-384).  ``workers``, ``layout`` and ``block_size`` are
+    accepted and have no effect on results, as in the reference;
+    ``parallel_cells`` runs the cells concurrently on the device (see
+    ``run_experiment``).
     """
 
     functions: Sequence[Union[str, BenchmarkFn]] = ("f1",)
@@ -246,15 +247,37 @@ def run_experiment(config: ExperimentConfig, out=None, summary_out=None) -> Expe
 
     A failure mid-experiment (e.g. ``NonFiniteFitnessError``) leaves the
     completed cells' rows plus a ``# FAILED`` marker, like the reference.
+    ``parallel_cells=True`` runs the cells concurrently, as the reference does
+    with a thread pool: each host thread drives its cell's batched launch on
+    its own CUDA stream, so the cells share the GPU's SMs (rows are still
+    written in cell order; wall times then include the contention, as the
+    reference warns).
     """
     functions = [_function(e, config.nvar) for e in config.functions]
+    cells = [(fn, schedule) for fn in functions for schedule in config.schedules]
     sink = _Rows(None if out is None else Path(out))
     records = []
+
+    def emit(recs):
+        for rec in recs:
+            sink.add(rec)
+            records.append(rec)
+
+    def one_cell(cell):
+        fn, schedule = cell
+        return run_cell(fn, config, range(config.replications), schedule)
+
     try:
-        for fn in functions:
-            for schedule in config.schedules:
+        if config.parallel_cells and len(cells) > 1:
+            from concurrent.futures import ThreadPoolExecutor
+
+            with ThreadPoolExecutor(max_workers=len(cells)) as pool:
+                for recs in pool.map(one_cell, cells):  # a failed cell raises here, in order
+                    emit(recs)
+        else:
+            for fn, schedule in cells:
                 try:
-                    cell = run_cell(fn, config, range(config.replications), schedule)
+                    cell = one_cell((fn, schedule))
                 except NonFiniteFitnessError:
                     # a batched cell fails as a whole: replay it run by run so the
                     # rows of the replications before the failing one are written
@@ -265,14 +288,10 @@ def run_experiment(config: ExperimentConfig, out=None, summary_out=None) -> Expe
                             one = run_cell(fn, replace(config, per_run_timing=True), [rid],
                                            schedule)
                         except NonFiniteFitnessError:
-                            for rec in cell:
-                                sink.add(rec)
-                                records.append(rec)
+                            emit(cell)
                             raise
                         cell.extend(one)
-                for rec in cell:
-                    sink.add(rec)
-                    records.append(rec)
+                emit(cell)
     except BaseException as exc:
         sink.failed(exc)
         raise

@@ -116,7 +116,7 @@ def test_run_experiment_both_schedules_match_reference_rows(tmp_path):
 def test_config_defaults_match_the_reference():
     c = H.ExperimentConfig()
     assert c.schedules == [ScheduleKind.SEQUENTIAL, ScheduleKind.PARALLEL]
-    assert H.ExperimentConfig(parallel_cells=True).parallel_cells is True  # accepted, no effect
+    assert H.ExperimentConfig(parallel_cells=True).parallel_cells is True  # concurrent cells
     assert c.per_run_timing is False
 
 
@@ -191,3 +191,19 @@ def test_trajectory_sidecar_round_trip_matches_reference_format(tmp_path):
     with pytest.raises(ValueError):
         (tmp_path / "e.txt").write_text("# columns\n")
         H.read_trajectory_rows(tmp_path / "e.txt")
+
+
+@pytest.mark.gpu
+def test_parallel_cells_run_concurrently_with_the_same_rows(tmp_path):
+    """parallel_cells=True (reference harness.py:236-242): cells on concurrent host threads,
+    each on its own CUDA stream -- the same records, in cell order."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    kw = dict(functions=["f1", "f4", "f5", "f7"], schedules=[ScheduleKind.SEQUENTIAL, ScheduleKind.PARALLEL],
+              replications=4, nsol=64, nvar=20, niter=50)
+    a = H.run_experiment(H.ExperimentConfig(**kw), out=tmp_path / "a.csv")
+    b = H.run_experiment(H.ExperimentConfig(parallel_cells=True, **kw), out=tmp_path / "b.csv")
+    key = lambda r: (r.function, str(r.schedule), r.run_id, r.seed, r.best_fitness)  # noqa: E731
+    assert [key(r) for r in a.records] == [key(r) for r in b.records]
+    assert len(b.records) == 4 * 2 * 4
