@@ -983,6 +983,20 @@ int fused_step(psso_ctx* c, int64_t t, int64_t* t_dev) {
 // number of swarms).  Else the global-memory exchange: RES when the tiles fit
 // and the B x G CTAs can be co-resident; else rows in HBM.  G = 1 needs no
 // co-residency.
+// Dynamic shared memory cap of a kernel.  The attribute is per function and
+// process-wide, so concurrent contexts (host threads running cells or seeds
+// side by side) would race if each set its own size: every caller sets the
+// device's opt-in maximum instead (the launch's own size decides occupancy),
+// after checking that its need fits.
+cudaError_t allow_smem(const void* f, size_t need) {
+  int dev = 0, optin = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  if (need > (size_t)optin) return cudaErrorInvalidValue;
+  return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+}
+
 bool plan_swarm(psso_ctx* c, int64_t B, SwarmPlan& sp, cudaError_t& e) {
   const psso_config* cfg = &c->cfg;
   const int64_t rows = cfg->row_hi - cfg->row_lo, D = cfg->nvar;
@@ -1012,7 +1026,7 @@ bool plan_swarm(psso_ctx* c, int64_t B, SwarmPlan& sp, cudaError_t& e) {
     const size_t smem = res_smem(gpc);
     const void* f = swarm_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, M, true, true);
     if (f && smem <= 227 * 1024) {
-      if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess ||
+      if ((e = allow_smem(f, smem)) != cudaSuccess ||
           (G > 8 && (e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess))
         return false;
       cudaLaunchConfig_t lc = {};
@@ -1042,7 +1056,7 @@ bool plan_swarm(psso_ctx* c, int64_t B, SwarmPlan& sp, cudaError_t& e) {
     const void* f = swarm_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, M, res, false);
     if (!f) return false;
     int per_sm = 0;
-    if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess ||
+    if ((e = allow_smem(f, smem)) != cudaSuccess ||
         (e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, PSSO_SWARM_NT, smem)) != cudaSuccess)
       return false;
     const int64_t cap = (int64_t)per_sm * c->num_sms;
@@ -1059,7 +1073,7 @@ bool plan_swarm(psso_ctx* c, int64_t B, SwarmPlan& sp, cudaError_t& e) {
   int per_sm = 0;                                                     // rows in HBM
   const void* f = swarm_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, M, false, false);
   if (!f) return false;
-  if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.off_xs)) != cudaSuccess ||
+  if ((e = allow_smem(f, sp.off_xs)) != cudaSuccess ||
       (e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, PSSO_SWARM_NT, sp.off_xs)) != cudaSuccess || per_sm < 1)
     return false;
   const int64_t cap = (int64_t)per_sm * c->num_sms;
@@ -1234,9 +1248,9 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
   cudaError_t e;
   if ((e = cudaGetDevice(&c->device)) != cudaSuccess ||
       (e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device)) != cudaSuccess ||
-      (e = cudaFuncSetAttribute(c->tile_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->L.smem)) != cudaSuccess ||
-      (e = cudaFuncSetAttribute(c->fused_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->LF.smem)) != cudaSuccess ||
-      (c->chain && (e = cudaFuncSetAttribute(c->init_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->init_smem)) != cudaSuccess)) {
+      (e = allow_smem(c->tile_fn, c->L.smem)) != cudaSuccess ||
+      (e = allow_smem(c->fused_fn, c->LF.smem)) != cudaSuccess ||
+      (c->chain && (e = allow_smem(c->init_fn, c->init_smem)) != cudaSuccess)) {
     delete c;
     return cuda_fail(nullptr, e, "psso_create");
   }
@@ -1590,7 +1604,7 @@ static cudaError_t launch_seq(psso_ctx* c, int M, SeqParams q, int64_t B, cudaSt
   if (res) smem = smem_res;
   const void* f = seq_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, M, res);
   if (!f) return cudaErrorInvalidDeviceFunction;
-  cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = allow_smem(f, smem);
   if (e == cudaSuccess && G > 8) e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t lc = {};
