@@ -993,8 +993,11 @@ cudaError_t allow_smem(const void* f, size_t need) {
   cudaError_t e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if (e != cudaSuccess) return e;
-  if (need > (size_t)optin) return cudaErrorInvalidValue;
-  return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+  cudaFuncAttributes fa;
+  if ((e = cudaFuncGetAttributes(&fa, f)) != cudaSuccess) return e;
+  const int cap = optin - (int)fa.sharedSizeBytes;  // dynamic + static <= opt-in maximum
+  if (need > (size_t)cap) return cudaErrorInvalidValue;
+  return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
 }
 
 bool plan_swarm(psso_ctx* c, int64_t B, SwarmPlan& sp, cudaError_t& e) {
