@@ -607,10 +607,6 @@ __global__ void k_rng(uint64_t seed, uint64_t stream, uint64_t t, const uint64_t
     out[k] = unit53(fold64(fold64(root, ii[k]), jj[k]));
 }
 
-__global__ void k_inv_sqrt(double* aux, int D) {  // 1.0 / np.sqrt(np.arange(1, D+1))
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < D; j += gridDim.x * blockDim.x)
-    aux[j] = __ddiv_rn(1.0, __dsqrt_rn((double)(j + 1)));
-}
 
 __global__ void k_set(int64_t* p, int64_t v) { *p = v; }
 __global__ void k_set_u64(unsigned long long* p, unsigned long long v) { *p = v; }
@@ -1370,8 +1366,13 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
       psso_destroy(c);
       return cuda_fail(nullptr, e, "psso_create aux");
     }
-    k_inv_sqrt<<<(int)((cfg->nvar + 255) / 256), 256>>>(c->aux, (int)cfg->nvar);
-    if ((e = cudaDeviceSynchronize()) != cudaSuccess) {
+    // 1.0 / np.sqrt(np.arange(1, D+1)) (benchmarks.py:216): IEEE sqrt and division
+    // are correctly rounded on host and device alike; copied, not computed on the
+    // device, so context creation never synchronizes the whole device
+    std::vector<double> inv((size_t)cfg->nvar);
+    for (int64_t j = 0; j < cfg->nvar; ++j) inv[(size_t)j] = 1.0 / std::sqrt((double)(j + 1));
+    if ((e = cudaMemcpy(c->aux, inv.data(), inv.size() * sizeof(double), cudaMemcpyHostToDevice)) !=
+        cudaSuccess) {
       psso_destroy(c);
       return cuda_fail(nullptr, e, "psso_create aux init");
     }
