@@ -136,3 +136,49 @@ def test_bench_gpus_2_self_spawns_and_bootstraps_the_nccl_communicator():
     assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
     assert out.stderr.count("library NCCL communicator unavailable") == 2  # both ranks, alike
     assert "torch.distributed all-gather" in d["config"]["parallelism"]
+
+
+def test_clock_samples_are_restricted_to_the_timed_region():
+    """ClockSampler keeps the samples nvidia-smi stamped inside [t0, t1] (the timed
+    region) and reports throttle reasons seen there; with none inside it falls back
+    to every sample and says so."""
+    import datetime
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("bench", ROOT / "bench.py")
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+
+    def stamp(ts):
+        return datetime.datetime.fromtimestamp(ts).strftime("%Y/%m/%d %H:%M:%S.%f")[:-3]
+
+    cs = bench.ClockSampler(0)
+    base = 1_800_000_000.0
+    rows = [(base - 1.0, "1000, 1965, 300, Not Active, Not Active, Not Active, Not Active"),
+            (base + 0.10, "1700, 1965, 990, Not Active, Not Active, Not Active, Active"),
+            (base + 0.12, "1650, 1965, 995, Not Active, Not Active, Not Active, Active"),
+            (base + 5.0, "1965, 1965, 100, Not Active, Not Active, Not Active, Not Active")]
+    import io
+
+    class P:  # a stand-in for the nvidia-smi process
+        stdout = io.StringIO("".join(f"{stamp(t)}, {r}\n" for t, r in rows))
+
+        def terminate(self):
+            pass
+
+        def wait(self, timeout=None):
+            pass
+
+    cs.proc = P()
+    cs._read()
+    cs.thread = type("T", (), {"join": lambda self, timeout=None: None})()
+    cs.t0, cs.t1 = base, base + 1.0
+    out = cs.stop()
+    assert out["window"] == "timed region" and out["samples"] == 2
+    assert out["sm_mhz"] == 1700.0 and out["reasons"] == ["sw_power_cap"]
+    cs2 = bench.ClockSampler(0)
+    cs2.lines = [(base + 9.0, rows[0][1])]
+    cs2.proc, cs2.thread = P(), cs.thread
+    cs2.t0, cs2.t1 = base, base + 1.0
+    out2 = cs2.stop()
+    assert out2["samples"] == 1 and out2["window"].startswith("timed region +")
