@@ -241,6 +241,27 @@ __device__ __forceinline__ Philox4 philox4x32_10(uint32_t c0, uint32_t c1, uint3
   return o;
 }
 
+// Two independent Philox4x32-10 calls with their rounds interleaved (same key):
+// twice the instruction-level parallelism of one serial 10-round chain.
+__device__ __forceinline__ void philox4x32_10_x2(uint32_t a0, uint32_t b0, uint32_t c1, uint32_t c2,
+                                                 uint32_t c3, uint32_t k0, uint32_t k1, Philox4& wa,
+                                                 Philox4& wb) {
+  uint32_t A0 = a0, A1 = c1, A2 = c2, A3 = c3;
+  uint32_t B0 = b0, B1 = c1, B2 = c2, B3 = c3;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t ha0 = __umulhi(0xD2511F53u, A0), la0 = 0xD2511F53u * A0;
+    const uint32_t ha1 = __umulhi(0xCD9E8D57u, A2), la1 = 0xCD9E8D57u * A2;
+    const uint32_t hb0 = __umulhi(0xD2511F53u, B0), lb0 = 0xD2511F53u * B0;
+    const uint32_t hb1 = __umulhi(0xCD9E8D57u, B2), lb1 = 0xCD9E8D57u * B2;
+    A0 = ha1 ^ A1 ^ k0; A2 = ha0 ^ A3 ^ k1; A1 = la1; A3 = la0;
+    B0 = hb1 ^ B1 ^ k0; B2 = hb0 ^ B3 ^ k1; B1 = lb1; B3 = lb0;
+    k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+  }
+  wa.w[0] = A0; wa.w[1] = A1; wa.w[2] = A2; wa.w[3] = A3;
+  wb.w[0] = B0; wb.w[1] = B1; wb.w[2] = B2; wb.w[3] = B3;
+}
+
 // ---------------------------------------------------------- vector I/O ----
 
 template <typename T, int V>
@@ -1090,6 +1111,9 @@ __device__ __forceinline__ T chain_term1(T x, T nb, int e) {
 #ifndef PSSO_CHAIN_MINB_F32
 #define PSSO_CHAIN_MINB_F32 PSSO_CHAIN_MINB  // resident CTAs per SM for the fp32 chain kernels
 #endif
+#ifndef PSSO_PHILOX_X2
+#define PSSO_PHILOX_X2 0  // chain kernels: two Philox calls with interleaved rounds
+#endif
 #ifndef PSSO_SWARM_PVJIT
 #define PSSO_SWARM_PVJIT 1  // k_swarm / k_seq with resident rows: pbests read from shared memory at
                             // their use (C2 f4 7.5 -> 6.8 us, f6 7.5 -> 7.2, f7 10.5 -> 10.2, C1 3.1 -> 3.0
@@ -1242,7 +1266,8 @@ __device__ __forceinline__ bool chain_step(const TileParams& p, const ChainEnv& 
       xb = xs30(fold64(ev.rootb, (uint64_t)gi));
       xf = xs30(fold64(ev.rootf, (uint64_t)gi));
     }
-    Philox4 w;  // RNG 1: one call per pair (m even, m + 1), see philox_pair
+    Philox4 w, w_next;  // RNG 1: one call per pair (m even, m + 1), see philox_pair;
+                        // PSSO_PHILOX_X2: pairs (m, m+2) computed together every 4 coordinates
 #pragma unroll
     for (int m = 0; m < M; ++m) {
       const int j = k + 8 * m;
@@ -1251,9 +1276,16 @@ __device__ __forceinline__ bool chain_step(const TileParams& p, const ChainEnv& 
       if (!FULL && 8 * m >= D) break;
       T v;
       if constexpr (RNG != 0) {
-        if ((m & 1) == 0)
+        if constexpr (PSSO_PHILOX_X2 && FULL && M % 4 == 0) {
+          if ((m & 3) == 0)
+            philox4x32_10_x2(philox_pair(j), philox_pair(j + 16), (uint32_t)gi, (uint32_t)(gi >> 32),
+                             (uint32_t)ev.t, (uint32_t)ev.seed, (uint32_t)(ev.seed >> 32), w, w_next);
+          else if ((m & 3) == 2)
+            w = w_next;
+        } else if ((m & 1) == 0) {
           w = philox4x32_10(philox_pair(j), (uint32_t)gi, (uint32_t)(gi >> 32), (uint32_t)ev.t,
                             (uint32_t)ev.seed, (uint32_t)(ev.seed >> 32));
+        }
       }
       if constexpr (RNG == 0) {
         const uint64_t gx = xg[j];
