@@ -262,6 +262,26 @@ __device__ __forceinline__ void philox4x32_10_x2(uint32_t a0, uint32_t b0, uint3
   wb.w[0] = B0; wb.w[1] = B1; wb.w[2] = B2; wb.w[3] = B3;
 }
 
+// Four independent calls, rounds interleaved (PSSO_PHILOX_X2 == 4).
+__device__ __forceinline__ void philox4x32_10_x4(const uint32_t (&a)[4], uint32_t c1, uint32_t c2,
+                                                 uint32_t c3, uint32_t k0, uint32_t k1, Philox4 (&w)[4]) {
+  uint32_t X0[4], X1[4], X2[4], X3[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) { X0[q] = a[q]; X1[q] = c1; X2[q] = c2; X3[q] = c3; }
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t h0 = __umulhi(0xD2511F53u, X0[q]), l0 = 0xD2511F53u * X0[q];
+      const uint32_t h1 = __umulhi(0xCD9E8D57u, X2[q]), l1 = 0xCD9E8D57u * X2[q];
+      X0[q] = h1 ^ X1[q] ^ k0; X2[q] = h0 ^ X3[q] ^ k1; X1[q] = l1; X3[q] = l0;
+    }
+    k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) { w[q].w[0] = X0[q]; w[q].w[1] = X1[q]; w[q].w[2] = X2[q]; w[q].w[3] = X3[q]; }
+}
+
 // ---------------------------------------------------------- vector I/O ----
 
 template <typename T, int V>
@@ -1267,6 +1287,7 @@ __device__ __forceinline__ bool chain_step(const TileParams& p, const ChainEnv& 
       xb = xs30(fold64(ev.rootb, (uint64_t)gi));
       xf = xs30(fold64(ev.rootf, (uint64_t)gi));
     }
+    Philox4 w4[4];  // PSSO_PHILOX_X2 == 4 only (unused otherwise)
     Philox4 w, w_next;  // RNG 1: one call per pair (m even, m + 1), see philox_pair;
                         // PSSO_PHILOX_X2: pairs (m, m+2) computed together every 4 coordinates
 #pragma unroll
@@ -1277,7 +1298,15 @@ __device__ __forceinline__ bool chain_step(const TileParams& p, const ChainEnv& 
       if (!FULL && 8 * m >= D) break;
       T v;
       if constexpr (RNG != 0) {
-        if constexpr (PSSO_PHILOX_X2 && FULL && M % 4 == 0) {
+        if constexpr (PSSO_PHILOX_X2 == 4 && FULL && M % 8 == 0) {
+          if ((m & 7) == 0) {
+            const uint32_t a[4] = {philox_pair(j), philox_pair(j + 16), philox_pair(j + 32),
+                                   philox_pair(j + 48)};
+            philox4x32_10_x4(a, (uint32_t)gi, (uint32_t)(gi >> 32), (uint32_t)ev.t, (uint32_t)ev.seed,
+                             (uint32_t)(ev.seed >> 32), w4);
+          }
+          if ((m & 1) == 0) w = w4[(m & 7) >> 1];
+        } else if constexpr (PSSO_PHILOX_X2 && FULL && M % 4 == 0) {
           if ((m & 3) == 0)
             philox4x32_10_x2(philox_pair(j), philox_pair(j + 16), (uint32_t)gi, (uint32_t)(gi >> 32),
                              (uint32_t)ev.t, (uint32_t)ev.seed, (uint32_t)(ev.seed >> 32), w, w_next);
