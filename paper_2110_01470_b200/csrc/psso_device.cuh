@@ -1131,9 +1131,6 @@ __device__ __forceinline__ T chain_term1(T x, T nb, int e) {
 #ifndef PSSO_CHAIN_MINB_F32
 #define PSSO_CHAIN_MINB_F32 PSSO_CHAIN_MINB  // resident CTAs per SM for the fp32 chain kernels
 #endif
-#ifndef PSSO_REF_X2
-#define PSSO_REF_X2 0  // chain kernels, reference RNG: two coordinates' hashes computed together
-#endif
 #ifndef PSSO_PHILOX_X2
 #define PSSO_PHILOX_X2 1  // chain / rows kernels: two Philox calls with interleaved rounds
                           // (C3 fp32 0.342 -> 0.331 ms; same stream)
@@ -1291,8 +1288,6 @@ __device__ __forceinline__ bool chain_step(const TileParams& p, const ChainEnv& 
       xf = xs30(fold64(ev.rootf, (uint64_t)gi));
     }
     Philox4 w4[4];  // PSSO_PHILOX_X2 == 4 only (unused otherwise)
-    uint64_t kb_pair[2];  // PSSO_REF_X2 only
-    double fr_pair[2];
     Philox4 w, w_next;  // RNG 1: one call per pair (m even, m + 1), see philox_pair;
                         // PSSO_PHILOX_X2: pairs (m, m+2) computed together every 4 coordinates
 #pragma unroll
@@ -1323,23 +1318,9 @@ __device__ __forceinline__ bool chain_step(const TileParams& p, const ChainEnv& 
         }
       }
       if constexpr (RNG == 0) {
-        uint64_t kb;
-        double fresh;
-        if constexpr (PSSO_REF_X2 && FULL && M % 2 == 0) {  // both coordinates' hashes together
-          if ((m & 1) == 0) {
-            const uint64_t gx0 = xg[j], gx1 = xg[j + 8];
-            kb_pair[0] = mix64_tail<(M <= 8 || sizeof(T) == 8)>(xb ^ gx0) >> 11;
-            kb_pair[1] = mix64_tail<(M <= 8 || sizeof(T) == 8)>(xb ^ gx1) >> 11;
-            fr_pair[0] = __dadd_rn(p.var_min, fresh_offset<(M <= 8 || sizeof(T) == 8)>(xf ^ gx0, p.span64));
-            fr_pair[1] = __dadd_rn(p.var_min, fresh_offset<(M <= 8 || sizeof(T) == 8)>(xf ^ gx1, p.span64));
-          }
-          kb = kb_pair[m & 1];
-          fresh = fr_pair[m & 1];
-        } else {
-          const uint64_t gx = xg[j];
-          kb = mix64_tail<(M <= 8 || sizeof(T) == 8)>(xb ^ gx) >> 11;
-          fresh = __dadd_rn(p.var_min, fresh_offset<(M <= 8 || sizeof(T) == 8)>(xf ^ gx, p.span64));
-        }
+        const uint64_t gx = xg[j];
+        const uint64_t kb = mix64_tail<(M <= 8 || sizeof(T) == 8)>(xb ^ gx) >> 11;
+        const double fresh = __dadd_rn(p.var_min, fresh_offset<(M <= 8 || sizeof(T) == 8)>(xf ^ gx, p.span64));
         v = x[m];
         v = kb >= p.Kw ? (PVJIT ? (j < D ? pjit[j] : (T)0) : pv[m]) : v;
         v = kb >= p.Kp ? gb[j] : v;
