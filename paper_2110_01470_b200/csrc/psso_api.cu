@@ -1189,7 +1189,7 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
     // the chain kernel's branch-free trig (psso_trig.cuh) is valid for
     // positions in a box of moderate size; wider boxes take the tile kernels
     const double box = std::max(std::fabs(cfg->var_min), std::fabs(cfg->var_max));
-    const bool trig_ok = box <= (cfg->dtype == PSSO_F64 ? kChainTrigMaxAbs : 1.0e6);
+    const bool trig_ok = box <= (cfg->dtype == PSSO_F64 ? kChainTrigMaxAbs : kChainTrigMaxAbsF32);
     if (M && terms_of(cfg->fn_id, D) <= 128 && trig_ok && !(off && *off && *off != '0')) {
       const bool full = D == 8 * M;
       const void* f = chain_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, M, false, full);
@@ -1224,7 +1224,7 @@ int psso_create(const psso_config* cfg, psso_ctx** out) {
     const int W = D == 512 ? 1 : D == 1024 ? 2 : D == 2048 ? 4 : D == 4096 ? 8 : 0;
     const char* off = std::getenv("PSSO_NO_ROWS");
     const double box = std::max(std::fabs(cfg->var_min), std::fabs(cfg->var_max));
-    const bool trig_ok = box <= (cfg->dtype == PSSO_F64 ? kChainTrigMaxAbs : 1.0e6);
+    const bool trig_ok = box <= (cfg->dtype == PSSO_F64 ? kChainTrigMaxAbs : kChainTrigMaxAbsF32);
     const void* f = W && trig_ok && !(off && *off && *off != '0')
                         ? rows_kernel(cfg->dtype, cfg->rng_mode, cfg->fn_id, W) : nullptr;
     if (f) {

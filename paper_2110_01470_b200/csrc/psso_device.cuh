@@ -346,51 +346,26 @@ __device__ __forceinline__ void stg_stream(T* p, const VecT<T, V>& v) {
 // Terms follow benchmarks.py:109-166 in numpy's elementwise order.
 
 // ---------------------------------------------------------- sin / cos ----
-// fp64 sin/cos for the objectives' moderate arguments: Cody-Waite reduction by
-// pi/2 with FMA (|y| <= 1e6) and the fdlibm __kernel_sin/__kernel_cos minimax
-// polynomials (|r| <= pi/4, < 1 ulp).  ~25 fp64 instructions instead of the
-// ~75 the general libdevice routine issues on this path; larger arguments
-// fall back to libdevice.  Agreement with glibc/numpy is to ulps either way
-// (the parity tolerance of the transcendental objectives).
-__device__ __forceinline__ void sincos_reduced(double y, double& s, double& c, int& q) {
-  const double t = __fma_rn(y, 6.36619772367581382433e-01, 6755399441055744.0);  // 1.5 * 2^52
-  const double kd = __dsub_rn(t, 6755399441055744.0);
-  q = __double2loint(t);
-  double r = __fma_rn(-kd, 1.5707963267948966, y);
-  r = __fma_rn(-kd, 6.123233995736766e-17, r);
-  const double z = __dmul_rn(r, r);
-  // sin(r) = r + r^3 (S1 + z (S2 + ... + z S6))
-  double ps = __fma_rn(z, 1.58969099521155010221e-10, -2.50507602534068634195e-08);
-  ps = __fma_rn(z, ps, 2.75573137070700676789e-06);
-  ps = __fma_rn(z, ps, -1.98412698298579493134e-04);
-  ps = __fma_rn(z, ps, 8.33333333332248946124e-03);
-  ps = __fma_rn(z, ps, -1.66666666666666324348e-01);
-  s = __fma_rn(__dmul_rn(z, r), ps, r);
-  // cos(r) = w + (((1 - w) - hz) + z^2 (C1 + z (C2 + ... + z C6))), w = 1 - z/2
-  double pc = __fma_rn(z, -1.13596475577881948265e-11, 2.08757232129817482790e-09);
-  pc = __fma_rn(z, pc, -2.75573143513906633035e-07);
-  pc = __fma_rn(z, pc, 2.48015872894767294178e-05);
-  pc = __fma_rn(z, pc, -1.38888888888741095749e-03);
-  pc = __fma_rn(z, pc, 4.16666666666666019037e-02);
-  const double hz = __dmul_rn(0.5, z);
-  const double w = __dsub_rn(1.0, hz);
-  c = __dadd_rn(w, __fma_rn(__dmul_rn(z, z), pc, __dsub_rn(__dsub_rn(1.0, w), hz)));
+// The objectives' sin/cos: the branch-free forms of psso_trig.cuh wherever
+// they are valid (|argument| <= trig_max: every position inside a box the
+// chain kernels accept), libdevice beyond.  Every kernel family -- chain,
+// rows, swarm, sequential, tile, fused and psso_eval_rows -- evaluates an
+// objective term with the same instructions, so re-evaluating a position on
+// the device returns its in-run fitness bit for bit (the reference's
+// `fn(best_position) == best_fitness`, test_core.py:168-174).
+template <typename T>
+__host__ __device__ constexpr double trig_max() {
+  return sizeof(T) == 8 ? kChainTrigMaxAbs : kChainTrigMaxAbsF32;
 }
-__device__ __forceinline__ double fast_cos(double y) {
-  if (!(fabs(y) <= 1.0e6)) return cos(y);
-  double s, c;
-  int q;
-  sincos_reduced(y, s, c, q);
-  const double v = (q & 1) ? s : c;
-  return ((q + 1) & 2) ? -v : v;
+template <typename T>
+__device__ __forceinline__ T obj_cos(T y) {
+  if constexpr (sizeof(T) == 8) return fabs(y) <= trig_max<T>() ? Trig<T>::cos_(y) : cos(y);
+  else return fabsf(y) <= (float)trig_max<T>() ? Trig<T>::cos_(y) : cosf(y);
 }
-__device__ __forceinline__ double fast_sin(double y) {
-  if (!(fabs(y) <= 1.0e6)) return sin(y);
-  double s, c;
-  int q;
-  sincos_reduced(y, s, c, q);
-  const double v = (q & 1) ? c : s;
-  return (q & 2) ? -v : v;
+template <typename T>
+__device__ __forceinline__ T obj_sin(T y) {
+  if constexpr (sizeof(T) == 8) return fabs(y) <= trig_max<T>() ? Trig<T>::sin_(y) : sin(y);
+  else return fabsf(y) <= (float)trig_max<T>() ? Trig<T>::sin_(y) : sinf(y);
 }
 
 template <typename T> struct Num;
@@ -399,8 +374,8 @@ template <> struct Num<double> {
   static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
   static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
   static __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
-  static __device__ __forceinline__ double cos_(double a) { return fast_cos(a); }
-  static __device__ __forceinline__ double sin_(double a) { return fast_sin(a); }
+  static __device__ __forceinline__ double cos_(double a) { return obj_cos(a); }
+  static __device__ __forceinline__ double sin_(double a) { return obj_sin(a); }
   static __device__ __forceinline__ double exp_(double a) { return exp(a); }
   static __device__ __forceinline__ double sqrt_(double a) { return __dsqrt_rn(a); }
   static __device__ __forceinline__ double pow4(double a) { return pow(a, 4.0); }
@@ -411,13 +386,40 @@ template <> struct Num<float> {
   static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
   static __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
   static __device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
-  static __device__ __forceinline__ float cos_(float a) { return cosf(a); }
-  static __device__ __forceinline__ float sin_(float a) { return sinf(a); }
+  static __device__ __forceinline__ float cos_(float a) { return obj_cos(a); }
+  static __device__ __forceinline__ float sin_(float a) { return obj_sin(a); }
   static __device__ __forceinline__ float exp_(float a) { return expf(a); }
   static __device__ __forceinline__ float sqrt_(float a) { return __fsqrt_rn(a); }
   static __device__ __forceinline__ float pow4(float a) { float s = a * a; return s * s; }
   static constexpr float TWO_PI = 6.2831855f;
 };
+
+// Rastrigin's term x*x - 10*cos(2*pi*x) (benchmarks.py:128-131) as
+// x*x + (-+10)*|cos(2*pi*x)| with the exact reduction of 2x, and Ackley's
+// cos(2*pi*x) (:132-140): the chain kernels' forms (no range check: their
+// box is inside trig_max), and the range-checked forms of the other kernels
+// (the same instructions inside trig_max, numpy's cos(fl(2*pi*x)) beyond).
+template <typename T>
+__device__ __forceinline__ T f5_term_in_range(T x) {
+  uint32_t odd;
+  const T p = Trig<T>::cos2pi_abs(x, odd);
+  const T c = Trig<T>::flip((T)-10, odd);
+  if constexpr (sizeof(T) == 8) return __fma_rn(p, c, __dmul_rn(x, x));
+  else return __fmaf_rn(p, c, __fmul_rn(x, x));
+}
+template <typename T>
+__device__ __forceinline__ T f5_term(T x) {
+  using N = Num<T>;
+  if (fabs((double)x) <= trig_max<T>()) return f5_term_in_range(x);
+  const T c = sizeof(T) == 8 ? (T)cos((double)N::mul((T)N::TWO_PI, x)) : (T)cosf((float)N::mul((T)N::TWO_PI, x));
+  return N::sub(N::mul(x, x), N::mul((T)10, c));
+}
+template <typename T>
+__device__ __forceinline__ T cos2pi_term(T x) {
+  using N = Num<T>;
+  if (fabs((double)x) <= trig_max<T>()) return Trig<T>::cos2pi(x);
+  return sizeof(T) == 8 ? (T)cos((double)N::mul((T)N::TWO_PI, x)) : (T)cosf((float)N::mul((T)N::TWO_PI, x));
+}
 
 // Objective terms, in numpy's elementwise order (benchmarks.py:109-166).
 // "Heavy" terms (transcendentals) may be precomputed by all threads into a
@@ -431,10 +433,9 @@ template <typename T, int FN>
 __device__ __forceinline__ T heavy_term(const T* x, int e) {
   using N = Num<T>;
   if constexpr (FN == 5) {
-    const T v = x[e];
-    return N::sub(N::mul(v, v), N::mul((T)10, N::cos_(N::mul((T)N::TWO_PI, v))));
+    return f5_term(x[e]);
   } else if constexpr (FN == 6) {
-    return N::cos_(N::mul((T)N::TWO_PI, x[e]));
+    return cos2pi_term(x[e]);
   } else if constexpr (FN == 8) {
     const T a = x[4 * e], b = x[4 * e + 1], c = x[4 * e + 2], d = x[4 * e + 3];
     const T t1 = N::add(a, N::mul((T)10, b));
@@ -1110,11 +1111,7 @@ __device__ __forceinline__ T chain_term1(T x, T nb, int e) {
     const T o = N::sub((T)1, x);
     return N::add(N::mul(N::mul((T)100, d), d), N::mul(o, o));
   } else if constexpr (FN == 5) {  // x*x - 10*cos(2*pi*x) as x*x + (-+10)*|cos|
-    uint32_t odd;
-    const T p = Trig<T>::cos2pi_abs(x, odd);
-    const T c = Trig<T>::flip((T)-10, odd);
-    if constexpr (sizeof(T) == 8) return __fma_rn(p, c, N::mul(x, x));
-    else return __fmaf_rn(p, c, N::mul(x, x));
+    return f5_term_in_range(x);
   } else if constexpr (FN == 9) {
     return N::mul(x, Trig<T>::sin_(N::sqrt_(fabs(x))));
   } else {  // 0, 1, 6, 7 (the x*x sum)

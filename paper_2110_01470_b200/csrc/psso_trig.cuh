@@ -149,5 +149,6 @@ template <> struct Trig<float> {
 
 // Largest |position| for which the chain kernel's trig is valid (host check).
 constexpr double kChainTrigMaxAbs = 1.0e12;
+constexpr double kChainTrigMaxAbsF32 = 1.0e6;  // fp32: |2x| < 2^22, Cody-Waite in fp32
 
 }  // namespace psso

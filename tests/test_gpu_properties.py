@@ -19,6 +19,7 @@ if not torch.cuda.is_available():  # pragma: no cover
 
 import paper_2110_01470_b200 as psso  # noqa: E402
 from oracle import oracle as O  # noqa: E402  (the checker)
+from paper_2110_01470_b200 import _lib  # noqa: E402
 from paper_2110_01470_b200.engine import DeviceEngine  # noqa: E402
 
 
@@ -253,3 +254,38 @@ def test_out_of_bounds_is_flagged_not_clamped():
     assert value == 36.0 and not in_bounds
     value, in_bounds = fn.evaluate_flagged(np.array([1.0, 0.0, 0.0]))
     assert value == 1.0 and in_bounds
+
+
+@pytest.mark.parametrize("fid,nsol,nvar,dtype,box,kernel", [
+    ("f5", 4096, 128, "float64", None, "k_chain"),
+    ("f5", 4096, 128, "float32", None, "k_chain"),
+    ("f6", 64, 1024, "float64", None, "k_rows"),
+    ("f7", 1000, 100, "float64", None, "k_swarm"),
+    ("f9", 1000, 100, "float64", None, "k_swarm"),
+    ("f6", 300, 300, "float64", None, "k_fused"),
+    ("f5", 200, 301, "float64", None, "k_tile"),
+    ("f5", 200, 301, "float32", None, "k_tile"),
+    ("f5", 4096, 128, "float64", 1e13, "k_fused"),
+])
+def test_reevaluated_pbests_equal_in_run_fitness(fid, nsol, nvar, dtype, box, kernel):
+    """test_core.py:168-174 (`fn(best_position) == best_fitness`) for every
+    kernel family: each pBest row re-evaluated by psso_eval_rows equals the
+    p_f the iteration kernel computed for it, bit for bit -- one set of
+    objective instructions on every device path (psso_device.cuh obj_cos)."""
+    fn = _fn(fid, nvar)
+    p = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=-box if box else fn.var_min,
+                       var_max=box if box else fn.var_max, nsol=nsol, nvar=nvar, niter=6)
+    eng = DeviceEngine(p, fn, 3, dtype=dtype)
+    try:
+        name = _lib.load().psso_kernel_name(eng.ctx).decode()
+        assert name.startswith(kernel), name
+        eng.initialize()
+        eng.run(0, p.niter)
+        eng.check()
+        sw = eng.to_host()
+        gf, gi = eng.result()
+    finally:
+        eng.close()
+    again = psso.benchmarks.evaluate_rows(fn, sw.pbests, dtype=dtype)
+    assert np.array_equal(again, sw.p_f)
+    assert psso.benchmarks.evaluate_rows(fn, sw.gbest[None, :], dtype=dtype)[0] == gf
