@@ -6,6 +6,7 @@
 // parallel.py:152-233; phases parallel.py:120-144; initialize core.py:196-210;
 // RngStream.uniform rng.py:73-87; BenchmarkFn.__call__ benchmarks.py:86-94.
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <chrono>
 #include <cmath>
@@ -931,6 +932,28 @@ struct DevGuard {
 };
 #define DEV_GUARD(c) DevGuard dev_guard_(c)
 
+// NVTX ranges (domain "psso") around the entry points that issue device work:
+// nvtx3 is header-only and does nothing unless a tool injects itself, so the
+// ranges cost one predictable branch per call.  Under ncu they scope captures
+// (`ncu --nvtx --nvtx-include "psso@psso_run/"`), under a timeline tool they
+// label the host spans of init / run / solve / exchange calls.
+struct NvtxRange {
+  static nvtxDomainHandle_t domain() {
+    static const nvtxDomainHandle_t d = nvtxDomainCreateA("psso");
+    return d;
+  }
+  explicit NvtxRange(const char* name) {
+    nvtxEventAttributes_t a = {};
+    a.version = NVTX_VERSION;
+    a.size = NVTX_EVENT_ATTRIB_STRUCT_SIZE;
+    a.messageType = NVTX_MESSAGE_TYPE_ASCII;
+    a.message.ascii = name;
+    nvtxDomainRangePushEx(domain(), &a);
+  }
+  ~NvtxRange() { nvtxDomainRangePop(domain()); }
+};
+#define TRACE(name) NvtxRange nvtx_range_(name)
+
 int need_bound(psso_ctx* c) {
   if (!c) return fail(nullptr, PSSO_E_INVALID, "null context");
   if (!c->bound) return fail(c, PSSO_E_INVALID, "context has no buffers bound (psso_bind)");
@@ -1465,6 +1488,7 @@ static int ensure_graph(psso_ctx* c) {
 
 int psso_init(psso_ctx* c) {
   DEV_GUARD(c);
+  TRACE("psso_init");
   if (int rc = need_bound(c)) return rc;
   k_set_u64<<<1, 1, 0, c->stream>>>(c->bad, ~0ull);
   c->launches++;
@@ -1478,6 +1502,7 @@ int psso_init(psso_ctx* c) {
 
 int psso_step(psso_ctx* c, int64_t t) {
   DEV_GUARD(c);
+  TRACE("psso_step");
   if (int rc = need_bound(c)) return rc;
   if (t < 0) return fail(c, PSSO_E_INVALID, "iteration must be >= 0");
   return fused_step(c, t, nullptr);
@@ -1557,6 +1582,7 @@ static int swarm_run(psso_ctx* c, int64_t t0, int64_t niter) {
 
 int psso_run(psso_ctx* c, int64_t t0, int64_t niter) {
   DEV_GUARD(c);
+  TRACE("psso_run");
   if (int rc = need_bound(c)) return rc;
   if (t0 < 0 || niter < 0) return fail(c, PSSO_E_INVALID, "t0 and niter must be >= 0");
   if (niter == 0) return PSSO_OK;
@@ -1707,6 +1733,7 @@ static int run_sequential_rows(psso_ctx* c, int64_t t0, int64_t niter) {
 
 int psso_run_sequential(psso_ctx* c, int64_t t0, int64_t niter) {
   DEV_GUARD(c);
+  TRACE("psso_run_sequential");
   if (int rc = need_bound(c)) return rc;
   if (t0 < 0 || niter < 0) return fail(c, PSSO_E_INVALID, "t0 and niter must be >= 0");
   const psso_config* cfg = &c->cfg;
@@ -1762,12 +1789,14 @@ int psso_sequential_passes(psso_ctx* c, int64_t* passes) {
 
 int psso_search(psso_ctx* c, int64_t t) {
   DEV_GUARD(c);
+  TRACE("psso_search");
   if (int rc = need_bound(c)) return rc;
   return launch_tile(c, tile_params(c, M_SEARCH, t, nullptr));
 }
 
 int psso_evaluate(psso_ctx* c, int64_t t) {
   DEV_GUARD(c);
+  TRACE("psso_evaluate");
   if (int rc = need_bound(c)) return rc;
   if (!c->buf.sol_f) return fail(c, PSSO_E_INVALID, "evaluate needs a sol_f buffer");
   return launch_tile(c, tile_params(c, M_LOAD | M_EVAL | M_SOLF, t < 0 ? -1 : t, nullptr));
@@ -1775,6 +1804,7 @@ int psso_evaluate(psso_ctx* c, int64_t t) {
 
 int psso_update_pbests(psso_ctx* c) {
   DEV_GUARD(c);
+  TRACE("psso_update_pbests");
   if (int rc = need_bound(c)) return rc;
   if (!c->buf.sol_f) return fail(c, PSSO_E_INVALID, "update_pbests needs a sol_f buffer");
   const int64_t rows = c->cfg.row_hi - c->cfg.row_lo;
@@ -1792,6 +1822,7 @@ int psso_update_pbests(psso_ctx* c) {
 
 int psso_update_gbest(psso_ctx* c) {
   DEV_GUARD(c);
+  TRACE("psso_update_gbest");
   if (int rc = need_bound(c)) return rc;
   const int64_t rows = c->cfg.row_hi - c->cfg.row_lo;
   k_argmin<<<c->argmin_grid, 256, 0, c->stream>>>(c->buf.p_f, rows, c->cfg.row_lo, c->slot_f, c->slot_i);
@@ -1822,6 +1853,7 @@ static int local_cand(psso_ctx* c, void* cand, int nslots) {
 
 int psso_init_local(psso_ctx* c, void* cand) {
   DEV_GUARD(c);
+  TRACE("psso_init_local");
   if (int rc = need_bound(c)) return rc;
   if (!cand) return fail(c, PSSO_E_INVALID, "null candidate buffer");
   k_set_u64<<<1, 1, 0, c->stream>>>(c->bad, ~0ull);
@@ -1833,6 +1865,7 @@ int psso_init_local(psso_ctx* c, void* cand) {
 
 int psso_step_local(psso_ctx* c, int64_t t, void* cand) {
   DEV_GUARD(c);
+  TRACE("psso_step_local");
   if (int rc = need_bound(c)) return rc;
   if (!cand) return fail(c, PSSO_E_INVALID, "null candidate buffer");
   if (int rc = launch_fused(c, t, nullptr)) return rc;
@@ -1841,6 +1874,7 @@ int psso_step_local(psso_ctx* c, int64_t t, void* cand) {
 
 int psso_apply_candidates(psso_ctx* c, int64_t t, const void* cands, int32_t ncand, int32_t is_init) {
   DEV_GUARD(c);
+  TRACE("psso_apply_candidates");
   if (int rc = need_bound(c)) return rc;
   if (!cands || ncand < 1) return fail(c, PSSO_E_INVALID, "need at least one candidate record");
   GbParams g = gb_params(c, t, nullptr, is_init, 0);
@@ -1927,6 +1961,7 @@ static int ensure_sgraph(psso_ctx* c);
 
 int psso_init_sharded(psso_ctx* c) {
   DEV_GUARD(c);
+  TRACE("psso_init_sharded");
   if (int rc = need_bound(c)) return rc;
   if (!c->comm) return fail(c, PSSO_E_INVALID, "no communicator (psso_attach_comm)");
   k_set_u64<<<1, 1, 0, c->stream>>>(c->bad, ~0ull);
@@ -1964,6 +1999,7 @@ static int ensure_sgraph(psso_ctx* c) {
 
 int psso_run_sharded(psso_ctx* c, int64_t t0, int64_t niter) {
   DEV_GUARD(c);
+  TRACE("psso_run_sharded");
   if (int rc = need_bound(c)) return rc;
   if (!c->comm) return fail(c, PSSO_E_INVALID, "no communicator (psso_attach_comm)");
   if (t0 < 0 || niter < 0) return fail(c, PSSO_E_INVALID, "t0 and niter must be >= 0");
@@ -2021,6 +2057,7 @@ int psso_p2p_close(void* dev_ptr) {
 int psso_publish_p2p(psso_ctx* c, const void* cand, void* const* peer_bufs, int32_t nranks,
                      int32_t rank, uint64_t epoch) {
   DEV_GUARD(c);
+  TRACE("psso_publish_p2p");
   if (int rc = need_bound(c)) return rc;
   if (!cand || !peer_bufs || nranks < 1 || rank < 0 || rank >= nranks || epoch == 0)
     return fail(c, PSSO_E_INVALID, "bad p2p publish arguments");
@@ -2036,6 +2073,7 @@ int psso_publish_p2p(psso_ctx* c, const void* cand, void* const* peer_bufs, int3
 int psso_apply_p2p(psso_ctx* c, int64_t t, const void* my_buf, int32_t nranks, uint64_t epoch,
                    int32_t is_init) {
   DEV_GUARD(c);
+  TRACE("psso_apply_p2p");
   if (int rc = need_bound(c)) return rc;
   if (!my_buf || nranks < 1 || epoch == 0) return fail(c, PSSO_E_INVALID, "bad p2p apply arguments");
   GbParams g = gb_params(c, t, nullptr, is_init, 0);
@@ -2076,6 +2114,7 @@ static int p2p_step_dev(psso_ctx* c, const void* peer_bufs, const PeerPtrs& pp, 
 int psso_run_p2p(psso_ctx* c, int64_t t0, int64_t niter, void* const* peer_bufs, const void* my_buf,
                  int32_t nranks, int32_t rank) {
   DEV_GUARD(c);
+  TRACE("psso_run_p2p");
   if (int rc = need_bound(c)) return rc;
   if (!peer_bufs || !my_buf || nranks < 1 || rank < 0 || rank >= nranks || t0 < 0 || niter < 0)
     return fail(c, PSSO_E_INVALID, "bad p2p loop arguments");
@@ -2246,6 +2285,7 @@ int psso_rng_uniform(uint64_t seed, uint64_t stream_key, uint64_t t, const uint6
 
 int psso_eval_rows(int32_t fn_id, int32_t dtype, int64_t nvar, const void* x, int64_t rows,
                    double* out, double probe_level, void* stream) {
+  TRACE("psso_eval_rows");
   psso_config cfg;
   std::memset(&cfg, 0, sizeof cfg);
   cfg.fn_id = fn_id;
@@ -2284,6 +2324,7 @@ int psso_eval_rows(int32_t fn_id, int32_t dtype, int64_t nvar, const void* x, in
 
 int psso_solve(const psso_config* cfg, int64_t niter, double* traj, void* best_position,
                double* best_fitness, double* wall_s) {
+  TRACE("psso_solve");
   // PSSO_SOLVE_TRACE=1: host time of each phase to stderr (diagnostic)
   const char* tr_env = std::getenv("PSSO_SOLVE_TRACE");
   const bool trace = tr_env && *tr_env && *tr_env != '0';
@@ -2543,12 +2584,14 @@ int psso_batch_failure(int64_t* swarm, int64_t* iteration, int64_t* particle, do
 
 int psso_solve_batch(const psso_config* cfg, const uint64_t* seeds, int32_t nseeds, int64_t niter,
                      double* traj, void* best_position, double* best_fitness, double* wall_s) {
+  TRACE("psso_solve_batch");
   return solve_batch(cfg, seeds, nseeds, niter, traj, best_position, best_fitness, wall_s, false);
 }
 
 int psso_solve_sequential_batch(const psso_config* cfg, const uint64_t* seeds, int32_t nseeds,
                                 int64_t niter, double* traj, void* best_position,
                                 double* best_fitness, double* wall_s) {
+  TRACE("psso_solve_sequential_batch");
   return solve_batch(cfg, seeds, nseeds, niter, traj, best_position, best_fitness, wall_s, true);
 }
 
