@@ -495,12 +495,10 @@ struct PeerPtrs {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(GB_THREADS) k_local_cand_publish(const __grid_constant__ GbParams g,
-                                                                   unsigned char* const* bufs,
-                                                                   const __grid_constant__ PeerPtrs pp,
-                                                                   int R, int rank, int64_t rec_bytes,
-                                                                   int64_t flag_bytes) {
-  const unsigned long long epoch = p2p_epoch(0, g.t_dev);
+__device__ __forceinline__ void local_cand_publish_body(const GbParams& g, unsigned char* const* bufs,
+                                                        const PeerPtrs& pp, int R, int rank,
+                                                        int64_t rec_bytes, int64_t flag_bytes,
+                                                        unsigned long long epoch) {
   const int slot = (int)(epoch & 1) * R + rank;  // records double-buffered by epoch parity
   // the record straight into this rank's slot of every buffer (R <= 64 ranks)
   __shared__ unsigned char* dst_s[64];
@@ -518,13 +516,20 @@ __global__ void __launch_bounds__(GB_THREADS) k_local_cand_publish(const __grid_
 }
 
 template <typename T>
-__global__ void __launch_bounds__(GB_THREADS) k_apply_p2p(const __grid_constant__ GbParams g,
-                                                          const unsigned char* buf, int R,
-                                                          unsigned long long epoch_arg, int64_t rec_bytes,
-                                                          int64_t flag_bytes) {
+__global__ void __launch_bounds__(GB_THREADS) k_local_cand_publish(const __grid_constant__ GbParams g,
+                                                                   unsigned char* const* bufs,
+                                                                   const __grid_constant__ PeerPtrs pp,
+                                                                   int R, int rank, int64_t rec_bytes,
+                                                                   int64_t flag_bytes) {
+  local_cand_publish_body<T>(g, bufs, pp, R, rank, rec_bytes, flag_bytes, p2p_epoch(0, g.t_dev));
+}
+
+template <typename T>
+__device__ __forceinline__ void apply_p2p_body(const GbParams& g, const unsigned char* buf, int R,
+                                               unsigned long long epoch, int64_t rec_bytes,
+                                               int64_t flag_bytes) {
   __shared__ int winner;
   __shared__ int take_s;
-  const unsigned long long epoch = p2p_epoch(epoch_arg, g.t_dev);
   // a rank can publish epoch e+1 before a slower rank applied epoch e, never
   // e+2 (that needs the slower rank's e+1 record): parity buffers suffice
   const int par = (int)(epoch & 1);
@@ -561,6 +566,31 @@ __global__ void __launch_bounds__(GB_THREADS) k_apply_p2p(const __grid_constant_
     T* dst = reinterpret_cast<T*>(g.gbest);
     copy_row<T>(src, g.D, [&](int j, T v) { dst[j] = v; });
   }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(GB_THREADS) k_apply_p2p(const __grid_constant__ GbParams g,
+                                                          const unsigned char* buf, int R,
+                                                          unsigned long long epoch_arg, int64_t rec_bytes,
+                                                          int64_t flag_bytes) {
+  apply_p2p_body<T>(g, buf, R, p2p_epoch(epoch_arg, g.t_dev), rec_bytes, flag_bytes);
+}
+
+// The device loop's whole exchange in ONE kernel: this rank's record, stored
+// into every rank's buffer with the epoch flags, then (same CTA) the wait for
+// every rank's flag, the lexicographic minimum and the gBest update.  Each
+// rank publishes before it waits, so the ranks' kernels cannot wait on each
+// other in a cycle; one launch per iteration fewer than publish + apply.
+template <typename T>
+__global__ void __launch_bounds__(GB_THREADS) k_p2p_exchange(const __grid_constant__ GbParams g,
+                                                             unsigned char* const* bufs,
+                                                             const __grid_constant__ PeerPtrs pp,
+                                                             const unsigned char* my_buf, int R, int rank,
+                                                             int64_t rec_bytes, int64_t flag_bytes) {
+  const unsigned long long epoch = p2p_epoch(0, g.t_dev);  // before apply advances t_dev
+  local_cand_publish_body<T>(g, bufs, pp, R, rank, rec_bytes, flag_bytes, epoch);
+  __syncthreads();
+  apply_p2p_body<T>(g, my_buf, R, epoch, rec_bytes, flag_bytes);
 }
 
 __global__ void k_argmin(const double* f, int64_t n, int64_t row_lo, double* slot_f,
@@ -2095,18 +2125,13 @@ static int p2p_step_dev(psso_ctx* c, const void* peer_bufs, const PeerPtrs& pp, 
   if (int rc = launch_fused(c, 0, c->t_dev)) return rc;
   const int64_t rb = psso_candidate_bytes(&c->cfg), fb = (int64_t)align16((size_t)nranks * 16);
   GbParams gl = gb_params(c, 0, c->t_dev, 0, c->fused_grid);
+  const auto bufs = (unsigned char* const*)peer_bufs;
+  const auto mine = (const unsigned char*)my_buf;
   if (c->cfg.dtype == PSSO_F64)
-    k_local_cand_publish<double><<<1, GB_THREADS, 0, c->stream>>>(gl, (unsigned char* const*)peer_bufs, pp,
-                                                                  nranks, rank, rb, fb);
+    k_p2p_exchange<double><<<1, GB_THREADS, 0, c->stream>>>(gl, bufs, pp, mine, nranks, rank, rb, fb);
   else
-    k_local_cand_publish<float><<<1, GB_THREADS, 0, c->stream>>>(gl, (unsigned char* const*)peer_bufs, pp,
-                                                                 nranks, rank, rb, fb);
-  GbParams g = gb_params(c, 0, c->t_dev, 0, 0);
-  if (c->cfg.dtype == PSSO_F64)
-    k_apply_p2p<double><<<1, GB_THREADS, 0, c->stream>>>(g, (const unsigned char*)my_buf, nranks, 0, rb, fb);
-  else
-    k_apply_p2p<float><<<1, GB_THREADS, 0, c->stream>>>(g, (const unsigned char*)my_buf, nranks, 0, rb, fb);
-  c->launches += 2;
+    k_p2p_exchange<float><<<1, GB_THREADS, 0, c->stream>>>(gl, bufs, pp, mine, nranks, rank, rb, fb);
+  c->launches += 1;
   CK(c, cudaGetLastError());
   return PSSO_OK;
 }
@@ -2140,7 +2165,7 @@ int psso_run_p2p(psso_ctx* c, int64_t t0, int64_t niter, void* const* peer_bufs,
   int64_t done = 0;
   const bool graph = c->stream != nullptr && !c->profiling;
   if (graph && niter >= GRAPH_CHUNK) {
-    if (!c->pgraph) {  // GRAPH_CHUNK x (fused kernel, record + publish, apply)
+    if (!c->pgraph) {  // GRAPH_CHUNK x (fused kernel, record + publish + wait + apply)
       cudaGraph_t gr;
       CK(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
       const int64_t saved = c->launches;
@@ -2160,7 +2185,7 @@ int psso_run_p2p(psso_ctx* c, int64_t t0, int64_t niter, void* const* peer_bufs,
     }
     for (; done + GRAPH_CHUNK <= niter; done += GRAPH_CHUNK) {
       CK(c, cudaGraphLaunch(c->pgraph, c->stream));
-      c->launches += 3 * GRAPH_CHUNK;
+      c->launches += 2 * GRAPH_CHUNK;
     }
   }
   for (; done < niter; ++done)  // same kernels, launched directly
