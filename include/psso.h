@@ -211,9 +211,10 @@ int psso_apply_p2p(psso_ctx* ctx, int64_t t, const void* my_buf, int32_t nranks,
                    int32_t is_init);
 
 /* Iterations t0..t0+niter-1 with the device-initiated exchange, replayed from
- * a captured CUDA graph of 16 iterations (fused kernel, record, publish,
- * apply; the epoch is t + 2, read from the device iteration counter, so the
- * graph needs no host values).  Initialize with psso_init_local +
+ * a captured CUDA graph of 16 iterations (per iteration the fused kernel and
+ * ONE exchange kernel: record, publish, wait for every rank's flag, apply;
+ * the epoch is t + 2, read from the device iteration counter, so the graph
+ * needs no host values).  Initialize with psso_init_local +
  * psso_publish_p2p / psso_apply_p2p at epoch 1.  `peer_bufs` (device array)
  * and `my_buf` as for psso_publish_p2p / psso_apply_p2p.  Asynchronous. */
 int psso_run_p2p(psso_ctx* ctx, int64_t t0, int64_t niter, void* const* peer_bufs, const void* my_buf,
