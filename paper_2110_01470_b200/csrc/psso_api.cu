@@ -485,9 +485,8 @@ __global__ void __launch_bounds__(GB_THREADS) k_publish(const unsigned char* can
   publish_body(cand, bufs, R, rank, p2p_epoch(epoch_arg, t_dev), rec_bytes, flag_bytes);
 }
 
-// the device loop's record + publish in one kernel: this rank's record (as
-// k_local_cand), then stored into every rank's buffer with the epoch flags
-// Up to 8 peers (a node's GPUs) travel by value in the launch parameters, so
+// The device loop's record + publish: this rank's record (as k_local_cand),
+// stored into every rank's buffer, then the epoch flags.  Up to 8 peers (a node's GPUs) travel by value in the launch parameters, so
 // the kernel starts without a dependent load of the peer table.
 struct PeerPtrs {
   unsigned char* p[8];
@@ -513,15 +512,6 @@ __device__ __forceinline__ void local_cand_publish_body(const GbParams& g, unsig
   if (threadIdx.x == 0)
     for (int q = 0; q < R; ++q)
       st_release_u64(reinterpret_cast<unsigned long long*>(dst[q]) + slot, epoch, R > 1);
-}
-
-template <typename T>
-__global__ void __launch_bounds__(GB_THREADS) k_local_cand_publish(const __grid_constant__ GbParams g,
-                                                                   unsigned char* const* bufs,
-                                                                   const __grid_constant__ PeerPtrs pp,
-                                                                   int R, int rank, int64_t rec_bytes,
-                                                                   int64_t flag_bytes) {
-  local_cand_publish_body<T>(g, bufs, pp, R, rank, rec_bytes, flag_bytes, p2p_epoch(0, g.t_dev));
 }
 
 template <typename T>
