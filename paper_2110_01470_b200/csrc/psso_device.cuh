@@ -1340,18 +1340,37 @@ __device__ __forceinline__ bool chain_step(const TileParams& p, const ChainEnv& 
   T* row = scr + (lane >> 3) * (8 * M);
   T prod = (T)1;
   if constexpr (FN == 7) {
-    // prod(cos(x_j / sqrt(j+1))) left to right (benchmarks.py:143-148): at
-    // each m the segment's 8 lanes hold j = 8m..8m+7, so every lane runs the
-    // same chain over shuffled factors -- no divergence, no smem round trip,
-    // and the factors of m+1 overlap the dependent multiplies of m
+    // prod(cos(x_j / sqrt(j+1))) left to right (benchmarks.py:143-148): the
+    // factors to the segment's smem row, then lane 0 of the segment runs the
+    // dependent multiplies over 16-byte loads issued ahead (4 loads per 8
+    // factors instead of 8 shuffles in every lane: C2 f7 10.2 -> 10.0 us per
+    // iteration) and shares the result
 #pragma unroll
     for (int m = 0; m < M; ++m) {
       if (!FULL && 8 * m >= D) break;
       const int j = k + 8 * m;
-      const T c = (FULL || j < D) ? Trig<T>::cos_(N::mul(x[m], (T)ev.aux[j])) : (T)1;  // x*1 == x
-#pragma unroll
-      for (int u = 0; u < 8; ++u) prod = N::mul(prod, __shfl_sync(0xffffffffu, c, seg + u));
+      if (FULL || j < D) row[j] = Trig<T>::cos_(N::mul(x[m], (T)ev.aux[j]));
     }
+    __syncwarp();
+    if (k == 0) {
+      using V4 = VecT<T, 16 / sizeof(T)>;
+      constexpr int PER = 16 / (int)sizeof(T);
+#pragma unroll
+      for (int g = 0; g < M; ++g) {
+        if (8 * g >= D) break;
+        T v[8];
+#pragma unroll
+        for (int h = 0; h < 8 / PER; ++h) {
+          const V4 q = reinterpret_cast<const V4*>(row + 8 * g)[h];
+#pragma unroll
+          for (int e = 0; e < PER; ++e) v[h * PER + e] = q.v[e];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (8 * g + u < D) prod = N::mul(prod, v[u]);
+      }
+    }
+    prod = __shfl_sync(0xffffffffu, prod, seg);
   } else if constexpr (chain_smem_fn<FN>()) {
 #pragma unroll
     for (int m = 0; m < M; ++m) {

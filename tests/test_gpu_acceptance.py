@@ -14,7 +14,7 @@ known failure: its band sits below the as-printed function's floor).
 """
 
 import warnings
-from concurrent.futures import ProcessPoolExecutor
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 import pytest
@@ -67,7 +67,7 @@ def precision_report():
 @pytest.fixture(scope="module")
 def oracle_finals():
     jobs = [(fid, sch, s) for fid in FIDS for sch in ("sequential", "parallel") for s in range(RUNS)]
-    with ProcessPoolExecutor(max_workers=O.max_threads()) as ex:
+    with ThreadPoolExecutor(max_workers=O.max_threads()) as ex:  # ctypes releases the GIL; no fork of a CUDA process
         out = list(ex.map(_oracle_run, jobs, chunksize=4))
     return {(j[0], j[1], j[2]): v for j, v in zip(jobs, out)}
 

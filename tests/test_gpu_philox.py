@@ -13,7 +13,7 @@ word 2 + h (fresh), or words 2h, 2h+1 as one 64-bit INIT draw.
 """
 
 import math
-from concurrent.futures import ProcessPoolExecutor
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 import pytest
@@ -87,7 +87,7 @@ def _oracle_final(args):
 def reference_finals():
     """The reference's final fitness (oracle, reference keyed RNG) for seeds 0..29 of the C2 suite."""
     jobs = [(fid, 1024, 100, 1000, s) for fid in ("f5", "f4", "f6", "f7") for s in range(30)]
-    with ProcessPoolExecutor(max_workers=O.max_threads()) as ex:
+    with ThreadPoolExecutor(max_workers=O.max_threads()) as ex:  # ctypes releases the GIL; no fork of a CUDA process
         out = list(ex.map(_oracle_final, jobs))
     return {fid: np.array(out[k * 30:(k + 1) * 30]) for k, fid in enumerate(("f5", "f4", "f6", "f7"))}
 
