@@ -75,12 +75,13 @@ def test_philox_stream_matches_random123_keying(fid, nsol, nvar):
 
 
 def _oracle_final(args):
-    fid, nsol, nvar, niter, seed = args
+    fid, nsol, nvar, niter, seed = args[:5]
+    sequential = len(args) > 5 and args[5]
     fn_box = {"f4": (-2.048, 2.048), "f5": (-5.12, 5.12), "f6": (-32.768, 32.768),
               "f7": (-600.0, 600.0)}[fid]
     o = O.Oracle(fid, nsol, nvar, 0.3, 0.6, 0.8, *fn_box, seed, threads=1)
     sw = o.initialize()
-    return o.run(sw, 0, niter)[-1]
+    return (o.run_sequential if sequential else o.run)(sw, 0, niter)[-1]
 
 
 @pytest.fixture(scope="module")
@@ -103,6 +104,34 @@ def test_philox_c2_suite_distribution_matches_reference(fid, dtype, reference_fi
     recs = psso.run_parallel_batch(p, fn, list(range(30)), dtype=dtype, rng="philox")  # one launch
     gpu = np.array([r.best_fitness for r in recs])
     ref = reference_finals[fid]
+    assert np.isfinite(gpu).all()
+    assert abs(gpu.mean() - ref.mean()) <= 0.10 * abs(ref.mean()), (gpu.mean(), ref.mean())
+    assert stats.kruskal(gpu, ref).pvalue > 0.01, (gpu, ref)
+    assert stats.ttest_ind(gpu, ref, equal_var=False).pvalue > 0.01, (gpu, ref)
+
+
+@pytest.fixture(scope="module")
+def reference_finals_sequential():
+    """The same for the reference's sequential schedule (core.py:213-258)."""
+    jobs = [(fid, 1024, 100, 1000, s, True) for fid in ("f5", "f4", "f6", "f7") for s in range(30)]
+    with ThreadPoolExecutor(max_workers=O.max_threads()) as ex:  # ctypes releases the GIL
+        out = list(ex.map(_oracle_final, jobs))
+    return {fid: np.array(out[k * 30:(k + 1) * 30]) for k, fid in enumerate(("f5", "f4", "f6", "f7"))}
+
+
+@pytest.mark.parametrize("fid", ["f5", "f4", "f6", "f7"])
+def test_philox_sequential_schedule_distribution_matches_reference(fid, reference_finals_sequential):
+    """Benchmark mode for the other schedule: run_sequential_batch (one k_seq
+    launch for 30 seeds) in Philox mode against the reference sequential
+    schedule's final fitness (oracle, reference RNG), same criteria."""
+    from scipy import stats
+
+    fn = psso.make_function(fid, 100)
+    p = psso.SsoParams(cw=0.3, cp=0.6, cg=0.8, var_min=fn.var_min, var_max=fn.var_max,
+                       nsol=1024, nvar=100, niter=1000)
+    recs = psso.run_sequential_batch(p, fn, list(range(30)), rng="philox")
+    gpu = np.array([r.best_fitness for r in recs])
+    ref = reference_finals_sequential[fid]
     assert np.isfinite(gpu).all()
     assert abs(gpu.mean() - ref.mean()) <= 0.10 * abs(ref.mean()), (gpu.mean(), ref.mean())
     assert stats.kruskal(gpu, ref).pvalue > 0.01, (gpu, ref)
